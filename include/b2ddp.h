@@ -1,0 +1,136 @@
+/*
+ * b2ddp.h — C-ABI of the B200-native hot paths of arXiv 2402.02447.
+ *
+ * The reference (ddpsim 0.1.0, /root/reference/pkg/src/ddpsim) is pure
+ * Python; its own boundary is the Python API re-exported at
+ * __init__.py:14-81.  Each entry point below replaces the inner loop of one
+ * reference function; the Python package paper_2402_02447_b200 keeps the
+ * reference names/signatures/errors on top of it (ctypes), and
+ * INTEGRATION.md shows the binding a maintainer would add.
+ *
+ * Conventions (all entry points):
+ *   - plain C types only; device buffers are caller-owned `void*`/typed
+ *     pointers; host arrays are marked [host];
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy stream);
+ *   - no allocation, no host synchronisation inside; kernels are enqueued
+ *     on `stream` and the call returns;
+ *   - return 0 (B2_OK) or a B2_ERR_* code; b2_last_error() returns a
+ *     thread-local message for the last failing call on this thread.
+ */
+#ifndef B2DDP_H_
+#define B2DDP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define B2_OK 0
+#define B2_ERR_INVALID 1      /* bad argument (pointer, size, dtype)          */
+#define B2_ERR_CUDA 2         /* CUDA runtime error (message has details)     */
+#define B2_ERR_INDIVISIBLE 3  /* seg_len % lanes != 0 (balance.py:65-66)       */
+#define B2_ERR_UNSUPPORTED 4  /* size beyond this build's limits              */
+
+/* element types */
+#define B2_F32 0
+#define B2_BF16 1
+#define B2_F64 2
+
+/* scan patterns (balance.py:21-23) */
+#define B2_SCAN_RASTER 0
+#define B2_SCAN_SNAKE 1
+
+const char* b2_version(void);
+const char* b2_last_error(void);
+
+/* ------------------------------------------------------------------------
+ * H1 — bucket-wise clip before allreduce
+ * ---------------------------------------------------------------------- */
+
+/* Bytes of scratch one b2_bucket_clip_cast caller (one stream) needs.  The
+ * buffer must be zeroed once (b2_clip_workspace_init); every launch leaves it
+ * zeroed again on exit, so it is reusable without re-initialisation. */
+size_t b2_clip_workspace_bytes(void);
+int b2_clip_workspace_init(void* workspace, size_t workspace_bytes, void* stream);
+
+/* K1 — fused per-bucket L2 norm + clip coefficient + scale/cast.
+ *
+ * Replaces clip_by_norm (gradsync.py:106-116) applied per (worker, bucket)
+ * inside sync_bucketwise (gradsync.py:157-160).  For every segment s (in the
+ * given order — pass buckets reversed to mirror gradsync.py:157):
+ *     norm_s  = sqrt(sum in[in_off[s] .. +len[s])^2)      (fp64 accumulation)
+ *     coef_s  = norm_s >= limit ? limit / norm_s : 1      (inclusive, :114)
+ *     out[out_off[s] + i] = cast(in[in_off[s] + i] * coef_s * post_scale)
+ * `out` may be NULL (norm/coef only).  `norms`, `coefs` (fp64) and `nonfinite`
+ * (int32, 1 if the segment holds inf/nan — gradsync.py:111-112) are optional
+ * device arrays of nseg entries.  in_dtype: B2_F32|B2_F64; out_dtype:
+ * B2_F32|B2_BF16|B2_F64.  post_scale folds 1/K in when the following
+ * collective is a plain sum.  ctas_per_sm <= 0 picks the default.
+ * seg_in_off/seg_out_off/seg_len are [host] arrays of nseg int64. */
+int b2_bucket_clip_cast(const void* in, int in_dtype, void* out, int out_dtype,
+                        const int64_t* seg_in_off, const int64_t* seg_out_off,
+                        const int64_t* seg_len, int nseg, double limit, double post_scale,
+                        double* norms, double* coefs, int32_t* nonfinite, void* workspace,
+                        size_t workspace_bytes, int ctas_per_sm, void* stream);
+
+/* K1b — single-process K-worker mean of clipped buckets.
+ *
+ * Replaces allreduce_mean (gradsync.py:119-128) over the clipped worker
+ * slices of sync_bucketwise (:158-161): for element i of bucket b,
+ *     out[i] = pairwise_tree_k( G[k*ld + i] * coef[k*B + b] ) / K
+ * with the reference's tree (rounds merge (0,1),(2,3).., odd tail carried).
+ * A coefficient of exactly 1 leaves the element untouched (clip_by_norm
+ * returns g itself, :116).  `bounds` is a [host] array of B+1 bucket edges
+ * (bounds[0] = 0, bounds[B] = D).  in_dtype B2_F32|B2_F64, out_dtype
+ * B2_F32|B2_F64; K <= 64. */
+int b2_weighted_mean(const void* G, int in_dtype, int64_t K, int64_t D, int64_t ld,
+                     const double* coef, const int64_t* bounds, int B, void* out,
+                     int out_dtype, void* stream);
+
+/* ------------------------------------------------------------------------
+ * H2 — stratified local presort
+ * ---------------------------------------------------------------------- */
+
+size_t b2_strata_workspace_bytes(int64_t n);
+
+/* K2 — stratum histogram + stable partition.
+ *
+ * Replaces stratify (strata.py:61-83): stratum of sample i is
+ * searchsorted(bounds, len[i], 'left') (:74); ids are emitted grouped by
+ * stratum, input order kept inside each stratum (:82).  `ids` may be NULL
+ * (ids = 0..n-1).  Outputs (device): ids_out[n], counts[nb] (int64), and
+ * bad[1] (int64) = first index i whose length is > bounds[nb-1] or < 1, or
+ * -1 (so the wrapper raises naming that sample's id, :75-80).  `bounds` is
+ * a [host] array of nb strictly ascending values >= 1, nb <= 16. */
+int b2_strata_partition(const int32_t* lengths, const int32_t* ids, int64_t n,
+                        const int32_t* bounds, int nb, int32_t* ids_out, int64_t* counts,
+                        int64_t* bad, void* workspace, size_t workspace_bytes, void* stream);
+
+/* K3 — per-pool stable sort by (-length, id) + raster/snake deal.
+ *
+ * Replaces _sorted_desc (balance.py:73-75) + _deal (:59-70) +
+ * _from_per_gpu (:54-56) as applied per node by assign_local_presort
+ * (:158-184) and, with one pool, by assign_global_presort (:83-88).
+ * ids/lens hold nseg consecutive pools of seg_len samples (each pool is the
+ * node's GPU draws concatenated in GPU order).  Outputs (device):
+ *   out_ids[nseg][lanes][seg_len/lanes]   (lane g's samples in deal order)
+ *   out_pos[nseg][lanes][seg_len/lanes] (may be NULL): flat input index of
+ *          each dealt sample (equal keys keep input order, i.e. stable)
+ *   tokens [nseg][lanes]  (int64 token sums, may be NULL)
+ *   bad[1] (int64, may be NULL): first flat index with len outside
+ *          [1, max_len] or id outside [0, max_id], else -1.
+ * max_len/max_id bound the key width (e.g. the last stratum boundary and the
+ * corpus size - 1).  seg_len % lanes != 0 -> B2_ERR_INDIVISIBLE.
+ * seg_len <= 4096. */
+int b2_presort_deal(const int32_t* ids, const int32_t* lens, int64_t nseg, int seg_len,
+                    int lanes, int scan, int32_t max_len, int32_t max_id, int32_t* out_ids,
+                    int32_t* out_pos, int64_t* tokens, int64_t* bad, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* B2DDP_H_ */

@@ -1,0 +1,56 @@
+"""B200-native hot paths of arXiv 2402.02447 behind the reference ``ddpsim`` API.
+
+H1 (bucket-wise clip before allreduce): ``gradsync`` + ``ddp`` (NCCL side
+stream, DDP comm hook).  H2 (stratified local presort): ``strata`` +
+``balance``.  All data passes run in ``_native/libb2ddp.so`` (sm_100a); see
+DESIGN.md.  Names mirror ``ddpsim/__init__.py:14-103`` for the in-scope paths.
+"""
+
+from .balance import Assignment, ScanPattern, assign_global_presort, assign_local_presort, presort_deal
+from .gradsync import (
+    BucketClipper,
+    ClipConfig,
+    ClipMode,
+    GradientState,
+    allreduce_mean,
+    capped_bucket_layout,
+    clip_by_norm,
+    equal_bucket_layout,
+    gradient_state_from_dict,
+    sync_after,
+    sync_before,
+    sync_bucketwise,
+    synchronize,
+)
+from .seqdata import (
+    DEFAULT_BIN_BOUNDARIES,
+    DEFAULT_BIN_PROBS,
+    MAX_SEQ_LEN,
+    LengthDistribution,
+    Sample,
+    Topology,
+    generate_corpus,
+    generate_lengths,
+)
+from .strata import (
+    DeviceStrata,
+    Strata,
+    StratumAllocation,
+    allocate_counts,
+    draw_batch,
+    stratify,
+    stratify_lengths,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "Assignment", "ScanPattern", "assign_global_presort", "assign_local_presort", "presort_deal",
+    "BucketClipper", "ClipConfig", "ClipMode", "GradientState", "allreduce_mean",
+    "capped_bucket_layout", "clip_by_norm", "equal_bucket_layout", "gradient_state_from_dict",
+    "sync_after", "sync_before", "sync_bucketwise", "synchronize",
+    "DEFAULT_BIN_BOUNDARIES", "DEFAULT_BIN_PROBS", "MAX_SEQ_LEN", "LengthDistribution",
+    "Sample", "Topology", "generate_corpus", "generate_lengths",
+    "DeviceStrata", "Strata", "StratumAllocation", "allocate_counts", "draw_batch",
+    "stratify", "stratify_lengths",
+]

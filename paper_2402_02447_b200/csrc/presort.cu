@@ -1,0 +1,163 @@
+// H2 / K3 — per-pool stable sort by (-length, id) + raster/snake deal (sm_100a).
+//
+// Reference: assign_local_presort (balance.py:158-184) pools each node's GPU
+// draws in GPU order (:179-182), sorts them with key (-length, id) using a
+// stable sort (_sorted_desc, :73-75), deals rows of `lanes` items, reversing
+// odd rows for SNAKE (_deal, :59-70), and sums lengths per lane
+// (_from_per_gpu, :54-56).  assign_global_presort (:83-88) is the same with a
+// single pool.
+//
+// One CTA per pool (grid-stride over pools).  The composite key
+//     ((max_len - len) << id_bits) | id
+// orders exactly like (-len, id); equal keys are identical samples, so the
+// order among them cannot change the output.  The key is sorted with an
+// in-register/shared-memory LSD radix sort limited to the bits the key
+// actually spans (cub::BlockRadixSort), then each sorted slot is dealt to
+// (lane, row) and staged in shared memory so the [lanes][rows] output tile is
+// written with consecutive addresses; token sums read the staged lengths.
+#include "common.cuh"
+
+#include <cub/block/block_radix_sort.cuh>
+
+#include <algorithm>
+#include <type_traits>
+
+namespace b2 {
+namespace {
+
+constexpr int kMaxSeg = 4096;
+
+struct PresortParams {
+  const int32_t* ids;
+  const int32_t* lens;
+  int64_t nseg;
+  int seg_len, lanes, rows, snake;
+  int32_t max_len, max_id;
+  int id_bits, end_bit;
+  int32_t* out_ids;
+  int32_t* out_pos;  // optional: flat input index of each dealt sample
+  int64_t* tokens;
+  int64_t* bad;
+};
+
+template <int T, int I, bool POS>
+__global__ void __launch_bounds__(T) k_presort_deal(const __grid_constant__ PresortParams p) {
+  // POS: carry each sample's input slot through the sort (a stable LSD radix
+  // sort keeps equal keys in input order, exactly like Timsort at :75)
+  using Sort = cub::BlockRadixSort<unsigned long long, T, I, typename std::conditional<POS, int32_t, cub::NullType>::type>;
+  __shared__ union {
+    typename Sort::TempStorage sort;
+    struct {
+      int32_t ids[T * I];   // dealt layout [lane][row]
+      int32_t lens[T * I];
+      int16_t pos[POS ? T * I : 1];  // slot within the pool (< 4096)
+    } stage;
+  } sm;
+  const unsigned long long idmask = (1ull << p.id_bits) - 1ull;
+  for (int64_t seg = blockIdx.x; seg < p.nseg; seg += gridDim.x) {
+    const int64_t base = seg * p.seg_len;
+    unsigned long long key[I];
+    int32_t slot[I];
+    long long first_bad = -1;
+#pragma unroll
+    for (int j = 0; j < I; ++j) {
+      const int i = threadIdx.x * I + j;  // blocked: keeps input order for stability
+      slot[j] = i;
+      if (i < p.seg_len) {
+        const int32_t L = p.lens[base + i], D = p.ids[base + i];
+        const bool ok = L >= 1 && L <= p.max_len && D >= 0 && D <= p.max_id;
+        if (!ok && first_bad < 0) first_bad = base + i;
+        key[j] = ((unsigned long long)(uint32_t)(p.max_len - L) << p.id_bits) | (unsigned long long)(uint32_t)D;
+      } else {
+        key[j] = ~0ull;  // padding sorts last (stable: after any equal real key)
+      }
+    }
+    if (first_bad >= 0 && p.bad) atomicMin(reinterpret_cast<unsigned long long*>(p.bad), (unsigned long long)first_bad);
+    if constexpr (POS) Sort(sm.sort).Sort(key, slot, 0, p.end_bit);
+    else Sort(sm.sort).Sort(key, 0, p.end_bit);
+    __syncthreads();  // sort temp storage -> staging buffer
+#pragma unroll
+    for (int j = 0; j < I; ++j) {
+      const int pos = threadIdx.x * I + j;
+      if (pos < p.seg_len) {
+        const int r = pos / p.lanes, c = pos - r * p.lanes;
+        const int lane = (p.snake && (r & 1)) ? p.lanes - 1 - c : c;  // balance.py:66-67
+        const int32_t id = (int32_t)(key[j] & idmask);
+        const int32_t len = p.max_len - (int32_t)(key[j] >> p.id_bits);
+        sm.stage.ids[lane * p.rows + r] = id;
+        sm.stage.lens[lane * p.rows + r] = len;
+        if constexpr (POS) sm.stage.pos[lane * p.rows + r] = (int16_t)slot[j];
+      }
+    }
+    __syncthreads();
+    int32_t* out = p.out_ids + base;
+    for (int i = threadIdx.x; i < p.seg_len; i += T) out[i] = sm.stage.ids[i];
+    if constexpr (POS)
+      for (int i = threadIdx.x; i < p.seg_len; i += T) p.out_pos[base + i] = (int32_t)base + sm.stage.pos[i];
+    if (p.tokens)
+      for (int l = threadIdx.x; l < p.lanes; l += T) {
+        int64_t s = 0;  // per-lane token sum (_from_per_gpu, balance.py:54-56)
+        for (int r = 0; r < p.rows; ++r) s += sm.stage.lens[l * p.rows + r];
+        p.tokens[seg * p.lanes + l] = s;
+      }
+    __syncthreads();  // staging / tok reused by the next pool
+  }
+}
+
+int bits_for(int64_t v) {  // bits needed to represent 0..v
+  int b = 0;
+  while (b < 63 && (1ll << b) <= v) ++b;
+  return b;
+}
+
+template <int T, int I>
+int launch(const PresortParams& p, cudaStream_t st) {
+  const DeviceInfo& di = device_info();
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(p.nseg, (int64_t)di.sm_count * 32));
+  if (p.out_pos) k_presort_deal<T, I, true><<<grid, T, 0, st>>>(p);
+  else k_presort_deal<T, I, false><<<grid, T, 0, st>>>(p);
+  B2_CHECK(cudaGetLastError());
+  return B2_OK;
+}
+
+}  // namespace
+}  // namespace b2
+
+using namespace b2;
+
+extern "C" int b2_presort_deal(const int32_t* ids, const int32_t* lens, int64_t nseg, int seg_len,
+                               int lanes, int scan, int32_t max_len, int32_t max_id,
+                               int32_t* out_ids, int32_t* out_pos, int64_t* tokens, int64_t* bad,
+                               void* stream) {
+  B2_REQUIRE(lanes >= 1, B2_ERR_INVALID, "lanes must be >= 1, got %d", lanes);
+  B2_REQUIRE(seg_len >= 0, B2_ERR_INVALID, "seg_len must be >= 0");
+  B2_REQUIRE(seg_len % lanes == 0, B2_ERR_INDIVISIBLE, "%d items do not divide over %d GPUs", seg_len, lanes);
+  B2_REQUIRE(seg_len <= kMaxSeg, B2_ERR_UNSUPPORTED, "seg_len %d exceeds %d", seg_len, kMaxSeg);
+  B2_REQUIRE(max_len >= 1 && max_id >= 0, B2_ERR_INVALID, "max_len must be >= 1 and max_id >= 0");
+  B2_REQUIRE(scan == B2_SCAN_RASTER || scan == B2_SCAN_SNAKE, B2_ERR_INVALID, "bad scan %d", scan);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (bad) B2_CHECK(cudaMemsetAsync(bad, 0xff, sizeof(int64_t), st));
+  if (nseg <= 0 || seg_len == 0) return B2_OK;
+  B2_REQUIRE(ids && lens && out_ids, B2_ERR_INVALID, "NULL pointer argument");
+  PresortParams p{};
+  p.ids = ids;
+  p.lens = lens;
+  p.nseg = nseg;
+  p.seg_len = seg_len;
+  p.lanes = lanes;
+  p.rows = seg_len / lanes;
+  p.snake = scan == B2_SCAN_SNAKE;
+  p.max_len = max_len;
+  p.max_id = max_id;
+  p.id_bits = std::max(1, bits_for(max_id));
+  p.end_bit = p.id_bits + std::max(1, bits_for((int64_t)max_len - 1));
+  p.out_ids = out_ids;
+  p.out_pos = out_pos;
+  p.tokens = tokens;
+  p.bad = bad;
+  B2_REQUIRE(p.end_bit <= 64, B2_ERR_UNSUPPORTED, "key does not fit 64 bits");
+  if (seg_len <= 128) return launch<32, 4>(p, st);
+  if (seg_len <= 512) return launch<128, 4>(p, st);
+  if (seg_len <= 2048) return launch<256, 8>(p, st);
+  return launch<512, 8>(p, st);
+}

@@ -1,0 +1,253 @@
+// H2 / K2 — stratum histogram + stable partition (sm_100a).
+//
+// Reference: stratify (strata.py:61-83): stratum of a sample is
+// searchsorted(bounds, length, side='left') (:74), samples are appended to
+// their stratum in input order (:81), probs = count/N (:82; host side).
+//
+// Three launches, all HBM/L2-streaming (8 B/key algorithmic: 4 B length read,
+// 4 B id written; +4 B if explicit ids are read):
+//   k_strata_count  : one CTA per 4096-key tile -> per-tile per-stratum counts
+//                     (+ first bad index via atomicMin)
+//   k_strata_scan   : one CTA, exclusive scan of tile counts per stratum,
+//                     stratum totals
+//   k_strata_scatter: one CTA per tile, stable in-tile ranks from a single
+//                     packed block scan (4 strata x 16-bit fields per u64),
+//                     staged through shared memory so each stratum's run is
+//                     written with consecutive addresses.
+#include "common.cuh"
+
+#include <cub/block/block_load.cuh>
+#include <cub/block/block_scan.cuh>
+
+#include <algorithm>
+
+namespace b2 {
+namespace {
+
+constexpr int kMaxStrata = 16;
+constexpr int kT = 256;            // threads per tile CTA
+constexpr int kItems = 16;         // keys per thread
+constexpr int kTile = kT * kItems; // 4096 keys per tile (fits 16-bit fields)
+
+struct StrataParams {
+  const int32_t* len;
+  const int32_t* ids;  // may be null: ids = index
+  int64_t n;
+  int nb;
+  int32_t bounds[kMaxStrata];
+  int32_t* tile_counts;  // [T][kMaxStrata]
+  int32_t* tile_off;     // [T][kMaxStrata] exclusive prefix over tiles
+  int64_t* counts;       // [nb] totals
+  int64_t* bad;          // first bad index (u64 min), pre-set to -1
+  int32_t* ids_out;
+};
+
+__device__ __forceinline__ int stratum_of(int32_t len, const StrataParams& p) {
+  int k = 0;
+#pragma unroll
+  for (int j = 0; j < kMaxStrata; ++j)
+    if (j < p.nb) k += (len > p.bounds[j]);  // == searchsorted(..., 'left')
+  return k;
+}
+
+template <int NW>
+struct Packed {
+  unsigned long long w[NW];
+  __device__ __forceinline__ Packed operator+(const Packed& o) const {
+    Packed r;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) r.w[i] = w[i] + o.w[i];
+    return r;
+  }
+  __device__ __forceinline__ unsigned field(int k) const {
+    return (unsigned)((w[k >> 2] >> ((k & 3) * 16)) & 0xffffull);
+  }
+};
+
+using LoadT = cub::BlockLoad<int32_t, kT, kItems, cub::BLOCK_LOAD_WARP_TRANSPOSE>;
+
+__global__ void __launch_bounds__(kT) k_strata_count(const __grid_constant__ StrataParams p) {
+  __shared__ typename LoadT::TempStorage ld;
+  __shared__ int cnt[kMaxStrata];
+  const int64_t base = (int64_t)blockIdx.x * kTile;
+  const int valid = (int)min64(kTile, p.n - base);
+  if (threadIdx.x < kMaxStrata) cnt[threadIdx.x] = 0;
+  int32_t v[kItems];
+  LoadT(ld).Load(p.len + base, v, valid, 1);
+  __syncthreads();
+  int local[kMaxStrata];
+#pragma unroll
+  for (int k = 0; k < kMaxStrata; ++k) local[k] = 0;
+  long long first_bad = -1;
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const int idx = threadIdx.x * kItems + j;
+    if (idx < valid) {
+      const int k = stratum_of(v[j], p);
+      const bool bad = (k == p.nb) || (v[j] < 1);
+      if (bad && first_bad < 0) first_bad = base + idx;
+#pragma unroll
+      for (int q = 0; q < kMaxStrata; ++q) local[q] += (!bad && q == k);
+    }
+  }
+  if (first_bad >= 0) atomicMin(reinterpret_cast<unsigned long long*>(p.bad), (unsigned long long)first_bad);
+#pragma unroll
+  for (int k = 0; k < kMaxStrata; ++k) {
+    if (k < p.nb) {
+      int s = local[k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if ((threadIdx.x & 31) == 0 && s) atomicAdd(&cnt[k], s);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < p.nb) p.tile_counts[(int64_t)blockIdx.x * kMaxStrata + threadIdx.x] = cnt[threadIdx.x];
+}
+
+// exclusive scan over tiles, per stratum; one CTA of 1024 threads
+__global__ void __launch_bounds__(1024) k_strata_scan(const __grid_constant__ StrataParams p, int64_t T) {
+  using Scan = cub::BlockScan<int64_t, 1024>;
+  __shared__ typename Scan::TempStorage ts;
+  for (int k = 0; k < p.nb; ++k) {
+    int64_t carry = 0;
+    for (int64_t t0 = 0; t0 < T; t0 += 1024) {
+      const int64_t t = t0 + threadIdx.x;
+      const int64_t c = t < T ? p.tile_counts[t * kMaxStrata + k] : 0;
+      int64_t ex, agg;
+      Scan(ts).ExclusiveSum(c, ex, agg);
+      if (t < T) p.tile_off[t * kMaxStrata + k] = (int32_t)(carry + ex);
+      carry += agg;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) p.counts[k] = carry;
+  }
+}
+
+template <int NW>
+__global__ void __launch_bounds__(kT) k_strata_scatter(const __grid_constant__ StrataParams p) {
+  using Scan = cub::BlockScan<Packed<NW>, kT>;
+  __shared__ union {
+    typename LoadT::TempStorage ld;
+    typename Scan::TempStorage scan;
+    int32_t stage[kTile];
+  } sm;
+  __shared__ int32_t s_kof[kTile];       // stratum of each staged slot
+  __shared__ int64_t s_dst[kMaxStrata];  // global start of this tile's run, per stratum
+  __shared__ int32_t s_lstart[kMaxStrata + 1];
+  const int64_t base = (int64_t)blockIdx.x * kTile;
+  const int valid = (int)min64(kTile, p.n - base);
+
+  int32_t v[kItems];
+  LoadT(sm.ld).Load(p.len + base, v, valid, 1);
+  __syncthreads();
+  int32_t id[kItems];
+  if (p.ids) {
+    LoadT(sm.ld).Load(p.ids + base, id, valid, 0);
+    __syncthreads();
+  } else {
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) id[j] = (int32_t)(base + threadIdx.x * kItems + j);
+  }
+  int8_t kk[kItems];
+  Packed<NW> mine;
+#pragma unroll
+  for (int i = 0; i < NW; ++i) mine.w[i] = 0;
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const int idx = threadIdx.x * kItems + j;
+    int k = -1;
+    if (idx < valid) {
+      k = stratum_of(v[j], p);
+      if (k == p.nb || v[j] < 1) k = -1;  // bad samples are reported, not placed
+    }
+    kk[j] = (int8_t)k;
+    if (k >= 0) mine.w[k >> 2] += 1ull << ((k & 3) * 16);
+  }
+  Packed<NW> ex, agg;
+  Scan(sm.scan).ExclusiveSum(mine, ex, agg);
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    int64_t gbase = 0;
+    for (int k = 0; k < p.nb; ++k) {
+      s_lstart[k] = acc;
+      acc += (int)agg.field(k);
+      s_dst[k] = gbase + p.tile_off[(int64_t)blockIdx.x * kMaxStrata + k];
+      gbase += p.counts[k];
+    }
+    s_lstart[p.nb] = acc;
+  }
+  __syncthreads();  // also retires the scan temp storage before staging
+  unsigned run[kMaxStrata];
+#pragma unroll
+  for (int k = 0; k < kMaxStrata; ++k) run[k] = 0;
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const int k = kk[j];
+    if (k >= 0) {
+      unsigned r = 0;
+#pragma unroll
+      for (int q = 0; q < kMaxStrata; ++q)
+        if (q == k) { r = run[q]; run[q] = r + 1; }
+      const int slot = s_lstart[k] + (int)ex.field(k) + (int)r;
+      sm.stage[slot] = id[j];
+      s_kof[slot] = k;
+    }
+  }
+  __syncthreads();
+  const int placed = s_lstart[p.nb];
+  for (int slot = threadIdx.x; slot < placed; slot += kT) {
+    const int k = s_kof[slot];
+    p.ids_out[s_dst[k] + (slot - s_lstart[k])] = sm.stage[slot];
+  }
+}
+
+}  // namespace
+}  // namespace b2
+
+using namespace b2;
+
+static inline int64_t strata_tiles(int64_t n) { return (n + kTile - 1) / kTile; }
+
+extern "C" size_t b2_strata_workspace_bytes(int64_t n) {
+  if (n < 1) n = 1;
+  return (size_t)strata_tiles(n) * kMaxStrata * sizeof(int32_t) * 2;
+}
+
+extern "C" int b2_strata_partition(const int32_t* lengths, const int32_t* ids, int64_t n,
+                                   const int32_t* bounds, int nb, int32_t* ids_out,
+                                   int64_t* counts, int64_t* bad, void* workspace,
+                                   size_t workspace_bytes, void* stream) {
+  B2_REQUIRE(lengths && ids_out && counts && bad && bounds, B2_ERR_INVALID, "NULL pointer argument");
+  B2_REQUIRE(n >= 1 && n <= INT32_MAX, B2_ERR_INVALID, "n must be in [1, 2^31-1], got %lld", (long long)n);
+  B2_REQUIRE(nb >= 1 && nb <= kMaxStrata, B2_ERR_UNSUPPORTED, "nb must be in [1, %d], got %d", kMaxStrata, nb);
+  B2_REQUIRE(bounds[0] >= 1, B2_ERR_INVALID, "boundaries must be >= 1");
+  for (int k = 1; k < nb; ++k)
+    B2_REQUIRE(bounds[k - 1] < bounds[k], B2_ERR_INVALID, "boundaries must be strictly ascending");
+  B2_REQUIRE(workspace && workspace_bytes >= b2_strata_workspace_bytes(n), B2_ERR_INVALID,
+             "strata workspace needs %zu bytes", b2_strata_workspace_bytes(n));
+  StrataParams p{};
+  p.len = lengths;
+  p.ids = ids;
+  p.n = n;
+  p.nb = nb;
+  for (int k = 0; k < kMaxStrata; ++k) p.bounds[k] = k < nb ? bounds[k] : INT32_MAX;
+  const int64_t T = strata_tiles(n);
+  p.tile_counts = static_cast<int32_t*>(workspace);
+  p.tile_off = p.tile_counts + T * kMaxStrata;
+  p.counts = counts;
+  p.bad = bad;
+  p.ids_out = ids_out;
+  cudaStream_t st = (cudaStream_t)stream;
+  B2_CHECK(cudaMemsetAsync(bad, 0xff, sizeof(int64_t), st));
+  k_strata_count<<<(unsigned)T, kT, 0, st>>>(p);
+  B2_CHECK(cudaGetLastError());
+  k_strata_scan<<<1, 1024, 0, st>>>(p, T);
+  B2_CHECK(cudaGetLastError());
+  const int nw = (nb + 3) / 4;
+  if (nw == 1) k_strata_scatter<1><<<(unsigned)T, kT, 0, st>>>(p);
+  else if (nw == 2) k_strata_scatter<2><<<(unsigned)T, kT, 0, st>>>(p);
+  else if (nw == 3) k_strata_scatter<3><<<(unsigned)T, kT, 0, st>>>(p);
+  else k_strata_scatter<4><<<(unsigned)T, kT, 0, st>>>(p);
+  B2_CHECK(cudaGetLastError());
+  return B2_OK;
+}

@@ -1,0 +1,338 @@
+"""H1 — bucket-wise gradient clipping before allreduce, on B200.
+
+Drop-in for the reference module ``ddpsim.gradsync`` (gradsync.py:1-191): the
+same names, arguments, modes and ``ValueError`` messages, but every pass over
+gradient data runs in the sm_100a kernels of ``_native/libb2ddp.so``:
+
+* K1 ``b2_bucket_clip_cast`` — per-bucket norm + clip coefficient + scale/cast
+  (clip_by_norm, gradsync.py:106-116, per worker and bucket as in :157-160);
+* K1b ``b2_weighted_mean`` — the K-worker pairwise-tree mean
+  (allreduce_mean, :119-128) for the single-process K>1 state.
+
+Array-like inputs (numpy, lists) are uploaded and results come back as fp64
+numpy arrays, like the reference.  CUDA tensors stay on the device (fp32 or
+fp64) and results are CUDA tensors.  ``BucketClipper`` is the low-level entry
+the DDP hook and the benchmark use (fp32 gradients -> bf16/fp32 comm buffer,
+no host synchronisation).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from enum import Enum
+from typing import Any, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+
+BERT_BUCKET_ELEMS = 25 * 1024 * 1024 // 4  # 25 MiB of fp32 = 6,553,600 elements
+
+
+class ClipMode(str, Enum):
+    AFTER_ALLREDUCE = "after_allreduce"
+    BEFORE_ALLREDUCE = "before_allreduce"
+    BUCKET_WISE = "bucket_wise"
+
+
+def equal_bucket_layout(dim: int, num_buckets: int) -> tuple:
+    """Contiguous equal ranges over [0, dim); the last one takes the remainder."""
+    if num_buckets < 1:
+        raise ValueError(f"num_buckets must be >= 1, got {num_buckets}")
+    if dim < num_buckets:
+        raise ValueError(f"cannot split dimension {dim} into {num_buckets} buckets")
+    step = dim // num_buckets
+    edges = [k * step for k in range(num_buckets)] + [dim]
+    return tuple((edges[k], edges[k + 1]) for k in range(num_buckets))
+
+
+def capped_bucket_layout(dim: int, bucket_elems: int = BERT_BUCKET_ELEMS) -> tuple:
+    """Fixed-capacity buckets (DDP-style 25 MiB fp32), the last one smaller."""
+    if dim < 1 or bucket_elems < 1:
+        raise ValueError("dim and bucket_elems must be >= 1")
+    return tuple((a, min(a + bucket_elems, dim)) for a in range(0, dim, bucket_elems))
+
+
+def _to_device_matrix(workers) -> tuple[torch.Tensor, bool]:
+    """(K, D) CUDA tensor + whether the caller handed us host data."""
+    if isinstance(workers, torch.Tensor):
+        host = not workers.is_cuda
+        t = workers
+        if t.dtype not in (torch.float32, torch.float64):
+            t = t.to(torch.float64)
+    else:
+        host = True
+        try:
+            arr = np.asarray(workers, dtype=float)
+        except ValueError:
+            raise ValueError("workers have mismatched dimensions") from None
+        t = torch.from_numpy(np.ascontiguousarray(arr))
+    if t.ndim != 2 or t.shape[0] < 1 or t.shape[1] < 1:
+        raise ValueError(f"expected a (workers, dim) matrix, got shape {tuple(t.shape)}")
+    _lib.load()
+    t = t.to("cuda", non_blocking=True).contiguous()
+    return t, host
+
+
+def _finite_or_raise(t: torch.Tensor, what: str) -> None:
+    if not bool(torch.isfinite(t).all()):
+        raise ValueError(f"{what} has non-finite components")
+
+
+@dataclass
+class GradientState:
+    """K per-worker flat gradients (rows of a CUDA matrix) + a bucket partition."""
+
+    workers: Any
+    bucket_layout: tuple
+
+    def __post_init__(self):
+        self.workers, self._host = _to_device_matrix(self.workers)
+        _finite_or_raise(self.workers, "gradient state")
+        layout = tuple((int(a), int(b)) for a, b in self.bucket_layout)
+        self.bucket_layout = layout
+        dim = self.workers.shape[1]
+        if not layout:
+            raise ValueError("bucket_layout must have at least one bucket")
+        edge = 0
+        for a, b in layout:
+            if a != edge or b <= a:
+                raise ValueError(
+                    f"bucket_layout must be disjoint contiguous ranges covering [0, {dim}), got {layout}"
+                )
+            edge = b
+        if edge != dim:
+            raise ValueError(f"bucket_layout covers [0, {edge}), expected [0, {dim})")
+
+    @property
+    def num_workers(self) -> int:
+        return self.workers.shape[0]
+
+    @property
+    def dim(self) -> int:
+        return self.workers.shape[1]
+
+    @property
+    def num_buckets(self) -> int:
+        return len(self.bucket_layout)
+
+
+def gradient_state_from_dict(doc: dict) -> GradientState:
+    """Build a state from a plain document (gradsync.py:81-92)."""
+    workers, _ = _to_device_matrix(doc["workers"])
+    if "bucket_layout" in doc:
+        layout = tuple((int(a), int(b)) for a, b in doc["bucket_layout"])
+    else:
+        layout = equal_bucket_layout(workers.shape[1], int(doc.get("num_buckets", 1)))
+    state = GradientState(workers, layout)
+    state._host = not isinstance(doc["workers"], torch.Tensor) or not doc["workers"].is_cuda
+    return state
+
+
+@dataclass(frozen=True)
+class ClipConfig:
+    threshold: float
+    mode: ClipMode
+
+    def __post_init__(self):
+        object.__setattr__(self, "mode", ClipMode(self.mode))
+        if not (self.threshold > 0 and math.isfinite(self.threshold)):
+            raise ValueError(f"threshold must be positive and finite, got {self.threshold}")
+
+
+# ---------------------------------------------------------------------------
+# low-level launcher (the hot path)
+
+_DT = {torch.float32: _lib.B2_F32, torch.bfloat16: _lib.B2_BF16, torch.float64: _lib.B2_F64}
+
+
+class BucketClipper:
+    """Launches K1 on one stream with its own zeroed workspace.
+
+    ``clip_cast(grad, out, segments, limit)`` enqueues one cooperative kernel
+    for all given segments (≤128 per launch); nothing synchronises the host.
+    ``segments`` is a sequence of (in_offset, out_offset, length).
+    """
+
+    def __init__(self, device=None, stream: torch.cuda.Stream | None = None, ctas_per_sm: int = 0):
+        self.lib = _lib.load()
+        self.device = torch.device(device if device is not None else "cuda")
+        self.stream = stream
+        self.ctas_per_sm = int(ctas_per_sm)
+        nbytes = self.lib.b2_clip_workspace_bytes()
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        _lib.check(self.lib.b2_clip_workspace_init(self.workspace.data_ptr(), nbytes, self._sp()))
+
+    def _sp(self) -> int:
+        return _lib.stream_ptr(self.stream)
+
+    def clip_cast(self, grad: torch.Tensor, out: torch.Tensor | None, segments: Sequence,
+                  limit: float, post_scale: float = 1.0, norms: torch.Tensor | None = None,
+                  coefs: torch.Tensor | None = None, nonfinite: torch.Tensor | None = None) -> None:
+        segs = list(segments)
+        if grad.dtype not in (torch.float32, torch.float64) or not grad.is_cuda:
+            raise ValueError("grad must be a CUDA float32/float64 tensor")
+        if out is not None and (out.dtype not in _DT or not out.is_cuda):
+            raise ValueError("out must be a CUDA float32/bfloat16/float64 tensor")
+        n_in = grad.numel()
+        for a, o, n in segs:
+            if a < 0 or n < 0 or a + n > n_in or (out is not None and (o < 0 or o + n > out.numel())):
+                raise ValueError(f"segment ({a}, {o}, {n}) is out of bounds")
+        for t in (norms, coefs):
+            if t is not None and (t.dtype != torch.float64 or t.numel() < len(segs)):
+                raise ValueError("norms/coefs must be float64 tensors with one entry per segment")
+        if nonfinite is not None and (nonfinite.dtype != torch.int32 or nonfinite.numel() < len(segs)):
+            raise ValueError("nonfinite must be an int32 tensor with one entry per segment")
+        ins = _lib.i64_array(s[0] for s in segs)
+        outs = _lib.i64_array(s[1] for s in segs)
+        lens = _lib.i64_array(s[2] for s in segs)
+        ws = self.workspace
+        rc = self.lib.b2_bucket_clip_cast(
+            grad.data_ptr(), _DT[grad.dtype],
+            out.data_ptr() if out is not None else None, _DT[out.dtype] if out is not None else 0,
+            ins, outs, lens, len(segs), float(limit), float(post_scale),
+            norms.data_ptr() if norms is not None else None,
+            coefs.data_ptr() if coefs is not None else None,
+            nonfinite.data_ptr() if nonfinite is not None else None,
+            ws.data_ptr(), ws.numel(), self.ctas_per_sm, self._sp(),
+        )
+        _lib.check(rc)
+
+    def weighted_mean(self, mat: torch.Tensor, coefs: torch.Tensor, bounds: Sequence[int],
+                      out: torch.Tensor) -> None:
+        K, D = mat.shape
+        b = _lib.i64_array(bounds)
+        rc = self.lib.b2_weighted_mean(
+            mat.data_ptr(), _DT[mat.dtype], K, D, mat.stride(0), coefs.data_ptr(), b,
+            len(bounds) - 1, out.data_ptr(), _DT[out.dtype], self._sp(),
+        )
+        _lib.check(rc)
+
+
+_clippers: dict = {}
+
+
+def _clipper() -> BucketClipper:
+    """One clipper (workspace) per (device, current stream)."""
+    s = torch.cuda.current_stream()
+    key = (s.device.index, int(s.cuda_stream))
+    c = _clippers.get(key)
+    if c is None:
+        c = _clippers[key] = BucketClipper(device=s.device, stream=s)
+    return c
+
+
+def _result(t: torch.Tensor, host: bool):
+    return t.cpu().numpy() if host else t
+
+
+def _raise_if_flagged(flags: torch.Tensor) -> None:
+    if bool(flags.any()):
+        raise ValueError("gradient has non-finite components")
+
+
+# ---------------------------------------------------------------------------
+# reference API
+
+
+def clip_by_norm(g, limit: float):
+    """Rescale g to L2 norm ``limit`` iff its norm reaches the limit (gradsync.py:106-116)."""
+    if limit <= 0:
+        raise ValueError(f"limit must be > 0, got {limit}")
+    if isinstance(g, torch.Tensor):
+        host = not g.is_cuda
+        v = g if g.dtype in (torch.float32, torch.float64) else g.to(torch.float64)
+    else:
+        host = True
+        v = torch.from_numpy(np.ascontiguousarray(np.asarray(g, dtype=float)))
+    src = v
+    v = v.reshape(-1).to("cuda").contiguous()
+    c = _clipper()
+    norms = torch.empty(1, dtype=torch.float64, device=v.device)
+    flags = torch.empty(1, dtype=torch.int32, device=v.device)
+    out = torch.empty_like(v)
+    c.clip_cast(v, out, [(0, 0, v.numel())], limit, norms=norms, nonfinite=flags)
+    _raise_if_flagged(flags)
+    if float(norms.item()) >= limit:
+        return _result(out.reshape(src.shape), host)
+    return src.numpy() if host else src  # unchanged: the input itself (:116)
+
+
+def allreduce_mean(workers):
+    """Elementwise mean over workers with the reference's pairwise tree (:119-128)."""
+    mat, host = _to_device_matrix(workers)
+    _finite_or_raise(mat, "gradient state")
+    out = torch.empty(mat.shape[1], dtype=mat.dtype, device=mat.device)
+    ones = torch.ones(mat.shape[0], dtype=torch.float64, device=mat.device)
+    _clipper().weighted_mean(mat, ones, [0, mat.shape[1]], out)
+    return _result(out, host)
+
+
+def _require_mode(cfg: ClipConfig, expected: ClipMode) -> None:
+    if cfg.mode is not expected:
+        raise ValueError(f"config mode is {cfg.mode.value}, expected {expected.value}")
+
+
+def sync_after(state: GradientState, cfg: ClipConfig):
+    """Mean of the full vectors, then clip the mean to c (:131-134)."""
+    _require_mode(cfg, ClipMode.AFTER_ALLREDUCE)
+    W = state.workers
+    c = _clipper()
+    mean = torch.empty(W.shape[1], dtype=W.dtype, device=W.device)
+    ones = torch.ones(W.shape[0], dtype=torch.float64, device=W.device)
+    c.weighted_mean(W, ones, [0, W.shape[1]], mean)
+    norms = torch.empty(1, dtype=torch.float64, device=W.device)
+    flags = torch.empty(1, dtype=torch.int32, device=W.device)
+    out = torch.empty_like(mean)
+    c.clip_cast(mean, out, [(0, 0, mean.numel())], cfg.threshold, norms=norms, nonfinite=flags)
+    _raise_if_flagged(flags)
+    return _result(out if float(norms.item()) >= cfg.threshold else mean, state._host)
+
+
+def sync_before(state: GradientState, cfg: ClipConfig):
+    """Clip every worker's full vector to c, then the pairwise mean (:137-145)."""
+    _require_mode(cfg, ClipMode.BEFORE_ALLREDUCE)
+    return _clip_then_mean(state, ((0, state.dim),), cfg.threshold)
+
+
+def sync_bucketwise(state: GradientState, cfg: ClipConfig):
+    """Clip each worker's bucket to c/sqrt(B), then average bucket by bucket (:148-162)."""
+    _require_mode(cfg, ClipMode.BUCKET_WISE)
+    limit = cfg.threshold / math.sqrt(state.num_buckets)
+    return _clip_then_mean(state, state.bucket_layout, limit)
+
+
+def _clip_then_mean(state: GradientState, layout, limit: float):
+    W = state.workers
+    K, D = W.shape
+    B = len(layout)
+    c = _clipper()
+    out = torch.empty(D, dtype=W.dtype, device=W.device)
+    flags = torch.empty(K * B, dtype=torch.int32, device=W.device)
+    if K == 1:
+        # one fused pass: norm + coef + scale straight into the result;
+        # buckets walked in reverse like a backward pass (:157)
+        segs = [(a, a, b - a) for a, b in reversed(layout)]
+        c.clip_cast(W, out, segs, limit, nonfinite=flags)
+    else:
+        coefs = torch.empty(K * B, dtype=torch.float64, device=W.device)
+        ld = W.stride(0)
+        segs = [(k * ld + a, 0, b - a) for k in range(K) for a, b in layout]
+        c.clip_cast(W, None, segs, limit, coefs=coefs, nonfinite=flags)
+        c.weighted_mean(W, coefs, [layout[0][0]] + [b for _, b in layout], out)
+    _raise_if_flagged(flags)
+    return _result(out, state._host)
+
+
+_SYNC_FNS = {
+    ClipMode.AFTER_ALLREDUCE: sync_after,
+    ClipMode.BEFORE_ALLREDUCE: sync_before,
+    ClipMode.BUCKET_WISE: sync_bucketwise,
+}
+
+
+def synchronize(state: GradientState, cfg: ClipConfig):
+    """Dispatch on cfg.mode (:165-174)."""
+    return _SYNC_FNS[cfg.mode](state, cfg)

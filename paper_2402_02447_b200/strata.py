@@ -1,0 +1,233 @@
+"""H2 — length strata, on B200 (drop-in for ``ddpsim.strata``, strata.py:1-161).
+
+* ``stratify`` / ``stratify_lengths`` run K2 ``b2_strata_partition`` (stratum
+  histogram + stable partition) on the device.  ``stratify`` keeps the
+  reference signature and returns ``Strata`` of ``Sample`` lists; the tensor
+  form returns ``DeviceStrata`` (partitioned int32 ids + counts) and never
+  leaves the GPU except for the ``nb`` stratum counts.
+* ``allocate_counts`` is four floats of host arithmetic (strata.py:86-110) and
+  stays on the host with the reference's exact numpy expression.
+* ``draw_batch`` is the boundary input: draws come from numpy's PCG64
+  ``Generator.choice`` (strata.py:113-161) and stay on the host so the draw
+  sequence is bit-identical; a device port is SURVEY §8(f) row 2.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from .seqdata import DEFAULT_BIN_BOUNDARIES, Sample
+
+DEFAULT_STRATUM_BOUNDARIES = DEFAULT_BIN_BOUNDARIES
+_I32_MAX = 2**31 - 1
+
+
+@dataclass
+class Strata:
+    """Per-stratum sample pools (mutated by draw_batch) + probabilities."""
+
+    boundaries: tuple
+    buckets: list
+    probs: tuple
+
+    @property
+    def num_strata(self) -> int:
+        return len(self.boundaries)
+
+    @property
+    def remaining(self) -> int:
+        return sum(len(pool) for pool in self.buckets)
+
+
+@dataclass(frozen=True)
+class StratumAllocation:
+    counts: tuple
+    local_batch: int
+
+    def __post_init__(self):
+        if any(c < 0 for c in self.counts):
+            raise ValueError(f"counts must be non-negative, got {self.counts}")
+        if sum(self.counts) != self.local_batch:
+            raise ValueError(
+                f"counts {self.counts} sum to {sum(self.counts)}, "
+                f"expected local_batch {self.local_batch}"
+            )
+
+
+@dataclass
+class DeviceStrata:
+    """Stratified ids resident in HBM: ``ids[offsets[k]:offsets[k]+counts[k]]`` is stratum k."""
+
+    boundaries: tuple
+    ids: torch.Tensor
+    counts: tuple
+    probs: tuple
+
+    @property
+    def offsets(self) -> tuple:
+        return tuple(int(x) for x in np.concatenate([[0], np.cumsum(self.counts)[:-1]]))
+
+    def pool(self, k: int) -> torch.Tensor:
+        o = self.offsets[k]
+        return self.ids[o : o + self.counts[k]]
+
+
+def _check_bounds(boundaries) -> tuple:
+    bounds = tuple(int(b) for b in boundaries)
+    if not bounds or bounds[0] < 1 or any(a >= b for a, b in zip(bounds, bounds[1:])):
+        raise ValueError(f"boundaries must be non-empty, ascending, >= 1: {bounds}")
+    if bounds[-1] > _I32_MAX:
+        raise ValueError(f"boundaries must fit int32: {bounds}")
+    return bounds
+
+
+def _partition(lengths: torch.Tensor, bounds: tuple, ids: torch.Tensor | None, stream=None):
+    """Launch K2; returns (ids_out, counts list, first bad index or -1)."""
+    lib = _lib.load()
+    n = lengths.numel()
+    dev = lengths.device
+    ws_bytes = lib.b2_strata_workspace_bytes(n)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    ids_out = torch.empty(n, dtype=torch.int32, device=dev)
+    counts = torch.empty(len(bounds), dtype=torch.int64, device=dev)
+    bad = torch.empty(1, dtype=torch.int64, device=dev)
+    rc = lib.b2_strata_partition(
+        lengths.data_ptr(), ids.data_ptr() if ids is not None else None, n,
+        _lib.i32_array(bounds), len(bounds), ids_out.data_ptr(), counts.data_ptr(),
+        bad.data_ptr(), ws.data_ptr(), ws_bytes, _lib.stream_ptr(stream),
+    )
+    _lib.check(rc)
+    host = torch.cat([bad, counts]).cpu().tolist()  # one D2H: nb + 1 integers
+    return ids_out, host[1:], host[0]
+
+
+def _as_i32_device(x, what: str) -> torch.Tensor:
+    t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(np.asarray(x)))
+    if t.dtype != torch.int32:
+        if t.numel() and (int(t.max()) > _I32_MAX or int(t.min()) < -_I32_MAX - 1):
+            raise ValueError(f"{what} must fit int32")
+        t = t.to(torch.int32)
+    return t.reshape(-1).to("cuda", non_blocking=True).contiguous()
+
+
+def stratify_lengths(lengths, boundaries=DEFAULT_STRATUM_BOUNDARIES, ids=None, stream=None) -> DeviceStrata:
+    """Tensor fast path of ``stratify``: lengths (and optional ids) -> DeviceStrata.
+
+    ids default to 0..n-1.  Raises like the reference for an empty corpus, a
+    sample beyond the last boundary (naming its id) or a length < 1.
+    """
+    bounds = _check_bounds(boundaries)
+    _lib.load()
+    lens = _as_i32_device(lengths, "lengths")
+    n = lens.numel()
+    if n == 0:
+        raise ValueError("cannot stratify an empty corpus")
+    idt = _as_i32_device(ids, "ids") if ids is not None else None
+    ids_out, counts, bad = _partition(lens, bounds, idt, stream)
+    if bad >= 0:
+        length = int(lens[bad])
+        sid = int(idt[bad]) if idt is not None else bad
+        if length < 1:
+            raise ValueError(f"sample length must be >= 1, got {length}")
+        raise ValueError(
+            f"sample id {sid} has length {length}, beyond the last stratum boundary {bounds[-1]}"
+        )
+    probs = tuple(int(c) / n for c in counts)
+    return DeviceStrata(boundaries=bounds, ids=ids_out, counts=tuple(int(c) for c in counts), probs=probs)
+
+
+def stratify(samples: Sequence[Sample], boundaries=DEFAULT_STRATUM_BOUNDARIES) -> Strata:
+    """Partition samples into strata by length, preserving input order (strata.py:61-83)."""
+    bounds = _check_bounds(boundaries)
+    if not samples:
+        raise ValueError("cannot stratify an empty corpus")
+    samples = list(samples)
+    lens = np.fromiter((s.length for s in samples), dtype=np.int64, count=len(samples))
+    # lengths beyond int32 are beyond every boundary: clamp, K2 reports them as bad
+    lens32 = np.minimum(lens, _I32_MAX).astype(np.int32)
+    _lib.load()
+    dev_lens = torch.from_numpy(lens32).to("cuda", non_blocking=True)
+    # the kernel partitions input slots; slots map back to the caller's Sample objects
+    slots, counts, bad = _partition(dev_lens, bounds, None)
+    if bad >= 0:
+        s = samples[bad]
+        raise ValueError(
+            f"sample id {s.id} has length {s.length}, beyond the last stratum boundary {bounds[-1]}"
+        )
+    order = slots.cpu().numpy()
+    buckets, o = [], 0
+    for c in counts:
+        buckets.append([samples[i] for i in order[o : o + c]])
+        o += c
+    total = len(samples)
+    return Strata(boundaries=bounds, buckets=buckets, probs=tuple(len(p) / total for p in buckets))
+
+
+def allocate_counts(probs: Sequence[float], local_batch: int) -> StratumAllocation:
+    """Largest-remainder apportionment, ties to the lower stratum (strata.py:86-110)."""
+    p = np.asarray(probs, dtype=float)
+    if p.ndim != 1 or p.size == 0:
+        raise ValueError("probs must be a non-empty 1-D sequence")
+    if (p < 0).any():
+        raise ValueError(f"negative probability in {probs}")
+    if local_batch < 0:
+        raise ValueError(f"local_batch must be >= 0, got {local_batch}")
+    total = p.sum()
+    if total <= 0:
+        raise ValueError("probabilities sum to zero")
+    quota = local_batch * p / total
+    base = np.floor(quota).astype(int)
+    extra = local_batch - int(base.sum())
+    if extra:
+        base[np.argsort(-(quota - base), kind="stable")[:extra]] += 1
+    return StratumAllocation(tuple(int(c) for c in base), local_batch)
+
+
+def draw_batch(strata: Strata, alloc: StratumAllocation, seed: int) -> list:
+    """Draw alloc.counts[k] samples per stratum without replacement (strata.py:113-141).
+
+    Host-side by design (numpy PCG64 stream = the reference's draws); pools
+    shrink across calls and a dry stratum borrows from the nonempty stratum
+    with the closest boundary.
+    """
+    if len(alloc.counts) != strata.num_strata:
+        raise ValueError(
+            f"allocation has {len(alloc.counts)} strata, corpus has {strata.num_strata}"
+        )
+    rng = np.random.default_rng(seed)
+    out: list = []
+
+    def pull(pool: list, take: int) -> None:
+        if take == 0:
+            return
+        # swap-pop in descending index order keeps lower indices valid (:147-152)
+        for i in sorted((int(i) for i in rng.choice(len(pool), size=take, replace=False)), reverse=True):
+            out.append(pool[i])
+            pool[i] = pool[-1]
+            pool.pop()
+
+    for k, need in enumerate(alloc.counts):
+        take = min(need, len(strata.buckets[k]))
+        pull(strata.buckets[k], take)
+        short = need - take
+        while short > 0:
+            cands = [
+                (abs(strata.boundaries[j] - strata.boundaries[k]), j)
+                for j in range(strata.num_strata)
+                if j != k and strata.buckets[j]
+            ]
+            if not cands:
+                raise ValueError(
+                    f"stratum {k + 1} exhausted and no other stratum can cover "
+                    f"the remaining {short} sample(s)"
+                )
+            j = min(cands)[1]
+            take = min(short, len(strata.buckets[j]))
+            pull(strata.buckets[j], take)
+            short -= take
+    return out

@@ -1,0 +1,246 @@
+"""H1 parity on the GPU: CUDA path vs the reference golden vectors and the oracle.
+
+Tolerances (north_star): norms and clipped gradients within 1e-5 relative in
+fp32 (max |diff| <= 1e-5 * max |ref|); the fp64 device path is held to 1e-12;
+a bf16 comm buffer is held to bf16 rounding (2^-8 relative per element).
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import ddp_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+from paper_2402_02447_b200 import (  # noqa: E402
+    BucketClipper,
+    ClipConfig,
+    GradientState,
+    allreduce_mean,
+    clip_by_norm,
+    equal_bucket_layout,
+    sync_after,
+    sync_before,
+    sync_bucketwise,
+    synchronize,
+)
+from paper_2402_02447_b200 import synthetic  # noqa: E402
+
+BUCKET = ClipConfig(1.0, "bucket_wise")
+BEFORE = ClipConfig(1.0, "before_allreduce")
+AFTER = ClipConfig(1.0, "after_allreduce")
+F32_REL = 1e-5
+
+
+def rel_err(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    scale = max(np.abs(b).max(), 1e-300)
+    return float(np.abs(a - b).max() / scale)
+
+
+def state(workers, buckets=1):
+    w = np.asarray(workers, dtype=float)
+    return GradientState(w, equal_bucket_layout(w.shape[1], buckets))
+
+
+# ------------------------------------------------------------- golden vectors
+def test_golden_fp64_path(h1_golden):
+    g = h1_golden
+    for i in range(int(g["n_cases"])):
+        w = g[f"c{i}_workers"]
+        layout = [tuple(x) for x in g[f"c{i}_layout"]]
+        out = sync_bucketwise(GradientState(w, layout), BUCKET)
+        assert isinstance(out, np.ndarray) and out.dtype == np.float64
+        np.testing.assert_allclose(out, g[f"c{i}_out"], rtol=1e-12, atol=1e-300)
+        if f"c{i}_before" in g:
+            np.testing.assert_allclose(sync_before(GradientState(w, layout), BEFORE), g[f"c{i}_before"], rtol=1e-12)
+            np.testing.assert_allclose(sync_after(GradientState(w, layout), AFTER), g[f"c{i}_after"], rtol=1e-12)
+
+
+def test_golden_fp32_device_path(h1_golden):
+    g = h1_golden
+    for i in range(int(g["n_cases"])):
+        w = g[f"c{i}_workers"]  # fp32-representable values
+        layout = [tuple(x) for x in g[f"c{i}_layout"]]
+        wt = torch.tensor(w, dtype=torch.float32, device="cuda")
+        out = sync_bucketwise(GradientState(wt, layout), BUCKET)
+        assert out.is_cuda and out.dtype == torch.float32
+        assert rel_err(out.cpu().numpy(), g[f"c{i}_out"]) <= F32_REL, i
+
+
+def test_golden_norms(h1_golden):
+    g = h1_golden
+    c = BucketClipper()
+    for i in range(int(g["n_cases"])):
+        w = g[f"c{i}_workers"]
+        layout = [tuple(x) for x in g[f"c{i}_layout"]]
+        K = w.shape[0]
+        for dt, tol in ((torch.float64, 1e-13), (torch.float32, 1e-12)):
+            wt = torch.tensor(w, dtype=dt, device="cuda")
+            segs = [(k * w.shape[1] + a, 0, b - a) for k in range(K) for a, b in layout]
+            norms = torch.empty(len(segs), dtype=torch.float64, device="cuda")
+            c.clip_cast(wt, None, segs, 0.5, norms=norms)
+            np.testing.assert_allclose(norms.cpu().numpy(), g[f"c{i}_norms"].ravel(), rtol=tol)
+
+
+# ------------------------------------------------------------- reference KATs
+def test_clip_kats():
+    np.testing.assert_allclose(clip_by_norm(np.array([3.0, 4.0]), 1.0), [0.6, 0.8], atol=1e-15)
+    g = np.array([3.0, 4.0])
+    np.testing.assert_array_equal(clip_by_norm(g, 10.0), g)
+    np.testing.assert_array_equal(clip_by_norm(np.zeros(4), 0.5), np.zeros(4))
+    # inclusive edge: norm == limit -> coefficient exactly 1 (test_gradsync.py:42-44)
+    np.testing.assert_array_equal(clip_by_norm(np.array([0.0, 2.0]), 2.0), [0.0, 2.0])
+    with pytest.raises(ValueError, match="non-finite"):
+        clip_by_norm(np.array([1.0, np.inf]), 1.0)
+    with pytest.raises(ValueError, match="non-finite"):
+        clip_by_norm(np.array([np.nan]), 1.0)
+    with pytest.raises(ValueError):
+        clip_by_norm(np.ones(2), 0.0)
+    # fp32 device tensor flavour of the inclusive edge
+    t = torch.tensor([0.0, 2.0], device="cuda")
+    assert torch.equal(clip_by_norm(t, 2.0), t)
+
+
+def test_allreduce_kats():
+    np.testing.assert_array_equal(allreduce_mean([[1.0, 2.0], [3.0, 4.0]]), [2.0, 3.0])
+    np.testing.assert_array_equal(allreduce_mean([[5.0, -1.0]]), [5.0, -1.0])
+    v = [1.5, 2.5, -3.0]
+    np.testing.assert_array_equal(allreduce_mean([v, v, v]), v)
+    with pytest.raises(ValueError, match="mismatch|matrix"):
+        allreduce_mean([[1.0, 2.0], [3.0]])
+    rng = np.random.default_rng(0)
+    for k in (1, 2, 3, 5, 8, 16):
+        w = rng.normal(size=(k, 33))
+        # the pairwise tree is the reference's: bit-identical to the oracle
+        np.testing.assert_array_equal(allreduce_mean(w), O.allreduce_mean(w))
+
+
+def test_bucketwise_kats():
+    out = sync_bucketwise(state([[3.0, 4.0] * 4], buckets=4), BUCKET)
+    np.testing.assert_allclose(out, [0.3, 0.4] * 4, atol=1e-15)
+    assert abs(np.linalg.norm(out) - 1.0) < 1e-12
+    np.testing.assert_array_equal(sync_bucketwise(state(np.zeros((3, 12)), 4), BUCKET), np.zeros(12))
+    st = GradientState(np.ones((2, 7)) * 10, equal_bucket_layout(7, 3))
+    assert np.linalg.norm(sync_bucketwise(st, BUCKET)) <= 1.0 + 1e-9
+    with pytest.raises(ValueError, match="mode"):
+        sync_after(state([[1.0, 2.0]]), BEFORE)
+    with pytest.raises(ValueError, match="non-finite"):
+        GradientState(np.array([[1.0, np.nan]]), ((0, 2),))
+    with pytest.raises(ValueError, match="non-finite"):
+        GradientState(torch.tensor([[1.0, float("inf")]], device="cuda"), ((0, 2),))
+
+
+def test_cross_mode_properties():
+    rng = np.random.default_rng(7)
+    for _ in range(60):
+        k = int(rng.choice([1, 4, 16]))
+        b = int(rng.choice([1, 4, 25]))
+        d = int(rng.integers(b, 300))
+        w = rng.normal(size=(k, d)) * float(rng.choice([0.01, 1.0, 100.0]))
+        out = sync_bucketwise(state(w, b), BUCKET)
+        assert np.linalg.norm(out) <= 1.0 + 1e-9
+        np.testing.assert_allclose(out, O.sync_bucketwise(w, equal_bucket_layout(d, b), 1.0), rtol=1e-12, atol=1e-300)
+    # B = 1 equals before-allreduce (acceptance criterion 2)
+    w = rng.normal(size=(4, 10)) * 3
+    np.testing.assert_allclose(sync_bucketwise(state(w, 1), BUCKET), sync_before(state(w), BEFORE), rtol=1e-12)
+    # below-threshold transparency is exact (test_gradsync.py:176-182)
+    w = rng.normal(size=(5, 12))
+    w *= 0.4 / (2 * np.sqrt(12) * np.abs(w).max())
+    np.testing.assert_array_equal(sync_bucketwise(state(w, 4), BUCKET), O.allreduce_mean(w))
+    # outlier bounded by c/K
+    for k in (2, 4, 16):
+        w = np.zeros((k, 8))
+        w[0] = 1e6
+        assert np.linalg.norm(sync_bucketwise(state(w, 4), BUCKET)) <= 1.0 / k + 1e-12
+    # dispatcher + bitwise determinism
+    w = rng.normal(size=(16, 40)) * 2
+    a = synchronize(state(w.copy(), 5), BUCKET)
+    b = sync_bucketwise(state(w.copy(), 5), BUCKET)
+    assert a.tobytes() == b.tobytes()
+
+
+# ------------------------------------------------------------- kernel edges
+def test_alignment_and_odd_sizes():
+    """Unaligned bases/offsets take the scalar path; odd lengths exercise head/tail."""
+    rng = np.random.default_rng(11)
+    c = BucketClipper()
+    base = torch.tensor(rng.normal(size=100_003) * 0.01, dtype=torch.float32, device="cuda")
+    for shift in (0, 1, 2, 3):
+        g = base[shift:]
+        n = g.numel()
+        layout = [(0, 7), (7, 4096 + 3), (4096 + 3, 50_001), (50_001, n)]
+        for odt in (torch.float32, torch.bfloat16):
+            out = torch.empty(n + 5, dtype=odt, device="cuda")[1:1 + n] if shift % 2 else torch.empty(n, dtype=odt, device="cuda")
+            norms = torch.empty(len(layout), dtype=torch.float64, device="cuda")
+            coefs = torch.empty_like(norms)
+            c.clip_cast(g, out, [(a, a, b - a) for a, b in layout], 0.3, norms=norms, coefs=coefs)
+            gh = g.double().cpu().numpy()
+            rn, rc = O.bucket_coefficients(gh, layout, 0.3)
+            np.testing.assert_allclose(norms.cpu().numpy(), rn, rtol=1e-12)
+            np.testing.assert_allclose(coefs.cpu().numpy(), rc, rtol=1e-12)
+            ref = np.concatenate([gh[a:b] * cf for (a, b), cf in zip(layout, rc)])
+            tol = F32_REL if odt == torch.float32 else 2.0 ** -8
+            assert rel_err(out.float().cpu().numpy(), ref) <= tol
+
+
+def test_workspace_reuse_and_determinism():
+    c = BucketClipper()
+    g = torch.randn(3_000_000, device="cuda") * 1e-3
+    layout = equal_bucket_layout(g.numel(), 7)
+    segs = [(a, a, b - a) for a, b in reversed(layout)]
+    first = None
+    for _ in range(40):
+        out = torch.empty_like(g)
+        norms = torch.empty(len(segs), dtype=torch.float64, device="cuda")
+        c.clip_cast(g, out, segs, 1.0 / math.sqrt(7), norms=norms)
+        cur = (out.cpu().numpy().tobytes(), norms.cpu().numpy().tobytes())
+        if first is None:
+            first = cur
+        assert cur == first
+
+
+def test_many_segments_multi_launch():
+    """> 128 segments are split over several launches; K x B segments for K=3."""
+    rng = np.random.default_rng(3)
+    w = rng.normal(size=(3, 300 * 5)) * 0.05
+    layout = equal_bucket_layout(w.shape[1], 300)
+    out = sync_bucketwise(GradientState(w, layout), BUCKET)
+    np.testing.assert_allclose(out, O.sync_bucketwise(w, layout, 1.0), rtol=1e-12, atol=1e-300)
+
+
+# ------------------------------------------------------------- full BASELINE sizes
+@pytest.mark.parametrize("dim", [synthetic.BERT_BASE_DIM, synthetic.BERT_LARGE_DIM])
+def test_bert_sized_parity(dim):
+    g, layout, scales = synthetic.bert_grads(dim)
+    B = len(layout)
+    limit = 1.0 / math.sqrt(B)
+    c = BucketClipper()
+    segs = [(a, a, b - a) for a, b in reversed(layout)]
+    norms = torch.empty(B, dtype=torch.float64, device="cuda")
+    coefs = torch.empty(B, dtype=torch.float64, device="cuda")
+    out32 = torch.empty_like(g)
+    c.clip_cast(g, out32, segs, limit, norms=norms, coefs=coefs)
+    out16 = torch.empty(dim, dtype=torch.bfloat16, device="cuda")
+    c.clip_cast(g, out16, segs, limit)
+    gh = g.cpu().numpy()
+    rnorm = np.array([np.linalg.norm(gh[a:b].astype(np.float64)) for a, b in reversed(layout)])
+    np.testing.assert_allclose(norms.cpu().numpy(), rnorm, rtol=1e-10)
+    rcoef = np.where(rnorm >= limit, limit / rnorm, 1.0)
+    np.testing.assert_allclose(coefs.cpu().numpy(), rcoef, rtol=1e-10)
+    clipped = rcoef < 1.0
+    assert 0 < clipped.sum() < B  # the seeded scale mix clips some buckets, not all
+    o32 = out32.cpu().numpy()
+    o16 = out16.float().cpu().numpy()
+    for (a, b), cf in zip(reversed(layout), rcoef):
+        ref = gh[a:b].astype(np.float64) * cf
+        assert rel_err(o32[a:b], ref) <= F32_REL
+        assert rel_err(o16[a:b], ref) <= 2.0 ** -8
+        # size-independent property: every clipped bucket lands on the limit
+        if cf < 1.0:
+            assert abs(np.linalg.norm(o32[a:b].astype(np.float64)) - limit) <= 1e-5 * limit
+    assert np.linalg.norm(o32.astype(np.float64)) <= 1.0 * (1 + 1e-5)

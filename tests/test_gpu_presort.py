@@ -1,0 +1,235 @@
+"""H2 parity on the GPU: K2 (strata partition) and K3 (presort + deal) are bit-exact.
+
+Pinned against the reference's golden vectors (tests/golden/h2_golden.json),
+the reference KATs, and the oracle at the BASELINE size (10M lengths over 8
+rank shards; a whole epoch of node-step pools).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import ddp_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+from paper_2402_02447_b200 import (  # noqa: E402
+    LengthDistribution,
+    Sample,
+    StratumAllocation,
+    Topology,
+    allocate_counts,
+    assign_global_presort,
+    assign_local_presort,
+    draw_batch,
+    generate_corpus,
+    presort_deal,
+    stratify,
+    stratify_lengths,
+)
+from paper_2402_02447_b200 import synthetic  # noqa: E402
+
+BOUNDS = (128, 256, 384, 512)
+
+
+def make(lengths):
+    return [Sample(i, int(x)) for i, x in enumerate(lengths)]
+
+
+# ------------------------------------------------------------- K2 stratify
+def test_stratify_golden(h2_golden):
+    for c in h2_golden["corpora"]:
+        samples = generate_corpus(LengthDistribution(), c["n"], c["seed"])
+        st = stratify(samples, BOUNDS)
+        assert [[s.id for s in p] for p in st.buckets] == c["pools"]
+        assert list(st.probs) == c["probs"]
+        assert list(allocate_counts(st.probs, 16).counts) == c["alloc16"]
+        ds = stratify_lengths(np.array(c["lengths"], dtype=np.int32), BOUNDS)
+        assert [ds.pool(k).cpu().tolist() for k in range(4)] == c["pools"]
+        assert list(ds.probs) == c["probs"]
+    e = h2_golden["edge_stratify"]
+    st = stratify(make(e["lengths"]), BOUNDS)
+    assert [[s.id for s in p] for p in st.buckets] == e["pools"]
+
+
+def test_stratify_kats():
+    st = stratify(make([100, 200, 300, 500]), BOUNDS)
+    assert [len(b) for b in st.buckets] == [1, 1, 1, 1] and st.probs == (0.25,) * 4
+    st = stratify(make([64] * 10), BOUNDS)
+    assert [len(b) for b in st.buckets] == [10, 0, 0, 0] and st.probs == (1.0, 0.0, 0.0, 0.0)
+    assert [len(b) for b in stratify(make([128, 129, 256, 257]), BOUNDS).buckets] == [1, 2, 1, 0]
+    st = stratify(make([10, 300, 20, 5, 290]), BOUNDS)
+    assert [s.id for s in st.buckets[0]] == [0, 2, 3] and [s.id for s in st.buckets[2]] == [1, 4]
+    with pytest.raises(ValueError, match="id 7"):
+        stratify([Sample(0, 100), Sample(7, 600)], BOUNDS)
+    with pytest.raises(ValueError):
+        stratify([], BOUNDS)
+    with pytest.raises(ValueError):
+        stratify(make([10]), (128, 64))
+    # first offending sample (input order) is the one named
+    with pytest.raises(ValueError, match="id 3 has length 700"):
+        stratify([Sample(9, 5), Sample(3, 700), Sample(4, 900)], BOUNDS)
+    with pytest.raises(ValueError, match="id 12345"):
+        lens = np.full(20000, 7, dtype=np.int32)
+        lens[12345] = 513
+        lens[19999] = 600
+        stratify_lengths(lens, BOUNDS)
+
+
+@pytest.mark.parametrize("n", [1, 4095, 4096, 4097, 100_003])
+@pytest.mark.parametrize("bounds", [BOUNDS, (512,), (10, 20, 30, 40, 50, 60, 70, 80, 90, 100, 200, 300, 400, 450, 500, 512)])
+def test_stratify_sizes_vs_oracle(n, bounds):
+    rng = np.random.default_rng(n + len(bounds))
+    lens = rng.integers(1, 513, size=n).astype(np.int32)
+    ids = rng.permutation(10 * n)[:n].astype(np.int32)
+    ds = stratify_lengths(lens, bounds, ids=ids)
+    pools, probs = O.stratify(lens, bounds, ids=ids)
+    assert ds.probs == probs
+    got = ds.ids.cpu().numpy()
+    np.testing.assert_array_equal(got, np.concatenate(pools))
+
+
+def test_stratify_full_config():
+    """10M Wikipedia-like lengths, 8 rank shards of 1.25M: bit-exact per shard."""
+    lens = synthetic_lengths()
+    shard = lens.size // 8
+    for r in range(8):
+        part = lens[r * shard:(r + 1) * shard]
+        ids = np.arange(r * shard, (r + 1) * shard, dtype=np.int32)
+        ds = stratify_lengths(part, BOUNDS, ids=ids)
+        pools, probs = O.stratify(part, BOUNDS, ids=ids)
+        assert ds.probs == probs
+        np.testing.assert_array_equal(ds.ids.cpu().numpy(), np.concatenate(pools))
+
+
+_LENS = None
+
+
+def synthetic_lengths():
+    global _LENS
+    if _LENS is None:
+        from paper_2402_02447_b200.seqdata import generate_lengths
+
+        _LENS = generate_lengths(LengthDistribution(), 10_000_000, 2402)
+    return _LENS
+
+
+# ------------------------------------------------------------- K3 presort + deal
+def test_local_presort_golden(h2_golden):
+    for c in h2_golden["local_presort"]:
+        draws = [[Sample(i, x) for i, x in zip(di, dl)] for di, dl in zip(c["draw_ids"], c["draw_lens"])]
+        a = assign_local_presort(draws, Topology(c["nodes"], c["gpn"]), c["scan"])
+        assert a.to_dict() == {"per_gpu_ids": c["per_gpu_ids"], "token_counts": c["token_counts"]}
+
+
+def test_global_presort_golden(h2_golden):
+    for c in h2_golden["global_presort"]:
+        samples = [Sample(i, x) for i, x in zip(c["ids"], c["lens"])]
+        a = assign_global_presort(samples, Topology(2, 4), c["scan"])
+        assert a.to_dict() == {"per_gpu_ids": c["per_gpu_ids"], "token_counts": c["token_counts"]}
+
+
+def test_presort_kats():
+    def draws(lengths, gpus, per_gpu):
+        s = make(lengths)
+        return [s[g * per_gpu:(g + 1) * per_gpu] for g in range(gpus)]
+
+    assert assign_local_presort(draws(range(16, 0, -1), 4, 4), Topology(1, 4), "snake").token_counts == (34,) * 4
+    assert assign_local_presort(draws(range(16, 0, -1), 4, 4), Topology(1, 4), "raster").token_counts == (40, 36, 32, 28)
+    a = assign_local_presort(draws([1, 2, 3, 4, 501, 502, 503, 504], 4, 2), Topology(2, 2), "snake")
+    assert {s.id for g in a.per_gpu[:2] for s in g} == {0, 1, 2, 3}
+    assert {s.id for g in a.per_gpu[2:] for s in g} == {4, 5, 6, 7}
+    a = assign_local_presort(draws([8, 6, 4, 2, 100, 75, 50, 25], 4, 2), Topology(2, 2), "snake")
+    assert sum(a.token_counts[:2]) == 20 and sum(a.token_counts[2:]) == 250
+    with pytest.raises(ValueError, match="differ"):
+        assign_local_presort([make([1, 2]), make([3])], Topology(1, 2), "snake")
+    with pytest.raises(ValueError):
+        assign_local_presort([make([1]), make([2])], Topology(1, 4), "snake")
+    g = assign_global_presort(make(range(16, 0, -1)), Topology(1, 4), "raster")
+    assert [s.length for s in g.per_gpu[0]] == [16, 12, 8, 4]
+    g = assign_global_presort(make([3, 16, 9, 1, 14, 2, 4, 15]), Topology(1, 2), "raster")
+    assert [s.length for s in g.per_gpu[0]] == [16, 14, 4, 2]
+    assert [[s.id for s in gpu] for gpu in assign_global_presort(make([9, 9, 9, 9]), Topology(1, 2), "raster").per_gpu] == [[0, 2], [1, 3]]
+    with pytest.raises(ValueError, match="divide"):
+        assign_global_presort(make([1, 2, 3]), Topology(1, 2))
+
+
+def test_duplicate_samples_stable():
+    """Identical (length, id) samples keep their input order (Timsort stability)."""
+    s = [Sample(5, 10), Sample(5, 10), Sample(1, 10), Sample(5, 10)]
+    a = assign_global_presort(s, Topology(1, 2), "raster")
+    ref = sorted(s, key=lambda x: (-x.length, x.id))
+    assert [x is y for x, y in zip([a.per_gpu[0][0], a.per_gpu[1][0], a.per_gpu[0][1], a.per_gpu[1][1]], ref)] == [True] * 4
+
+
+@pytest.mark.parametrize("seg_len,lanes", [(8, 8), (128, 8), (384, 8), (96, 4), (500, 5), (2048, 8), (4096, 64), (3000, 3)])
+@pytest.mark.parametrize("snake", [True, False])
+def test_presort_deal_vs_oracle(seg_len, lanes, snake):
+    rng = np.random.default_rng(seg_len * 7 + lanes)
+    nseg = max(1, 20000 // seg_len)
+    lens = rng.integers(1, 513, size=nseg * seg_len).astype(np.int32)
+    ids = rng.integers(0, 50_000, size=nseg * seg_len).astype(np.int32)  # repeats allowed
+    out, tok, _, bad = presort_deal(torch.from_numpy(ids).cuda(), torch.from_numpy(lens).cuda(),
+                                    seg_len, lanes, "snake" if snake else "raster", max_len=512, max_id=49_999)
+    assert int(bad) == -1
+    ro, rt = O.presort_deal_segments(ids, lens, seg_len, lanes, snake)
+    np.testing.assert_array_equal(out.cpu().numpy(), ro)
+    np.testing.assert_array_equal(tok.cpu().numpy(), rt)
+
+
+def test_presort_full_epoch_vs_oracle():
+    """BASELINE config: Topology(1, 8), lb 16 / 48, one epoch of node-step pools."""
+    lens = synthetic_lengths()
+    shard = lens.size // 8
+    for lb in (16, 48):
+        ids_r, lens_r = [], []
+        for r in range(8):
+            part = lens[r * shard:(r + 1) * shard]
+            _, probs = O.stratify(part)
+            counts = O.allocate_counts(probs, lb)
+            i, l = synthetic.epoch_draws(part, (128, 256, 384, 512), counts, None, seed=100 + r)
+            ids_r.append(i + r * shard)
+            lens_r.append(l)
+        steps = min(x.shape[0] for x in ids_r)
+        # pool of step t = GPU0's draw, GPU1's draw, ... (balance.py:179-182)
+        ids = np.stack([x[:steps] for x in ids_r], axis=1).reshape(-1)
+        ln = np.stack([x[:steps] for x in lens_r], axis=1).reshape(-1)
+        out, tok, _, bad = presort_deal(torch.from_numpy(ids).cuda(), torch.from_numpy(ln).cuda(),
+                                        8 * lb, 8, "snake", max_len=512, max_id=lens.size - 1)
+        assert int(bad) == -1
+        ro, rt = O.presort_deal_segments(ids, ln, 8 * lb, 8, True)
+        np.testing.assert_array_equal(out.cpu().numpy(), ro)
+        np.testing.assert_array_equal(tok.cpu().numpy(), rt)
+        # size-independent: every id appears exactly once across the epoch
+        assert np.unique(out.cpu().numpy()).size == ids.size
+
+
+def test_mcsim_second_oracle(h2_golden):
+    """Token counts of mcsim's LOCAL_PRESORT trial (mcsim.py:201-212) from K3."""
+    for c in h2_golden["mcsim"]:
+        mat = np.array(c["mat"], dtype=np.int32)  # (b, G) lengths
+        b, G = mat.shape
+        gpn, nodes = c["gpn"], c["nodes"]
+        pools = mat.reshape(b, nodes, gpn).transpose(1, 0, 2).reshape(-1)
+        ids = np.arange(pools.size, dtype=np.int32)
+        _, tok, _, _ = presort_deal(torch.from_numpy(ids).cuda(), torch.from_numpy(pools).cuda(),
+                                    b * gpn, gpn, c["scan"], max_len=512, max_id=pools.size)
+        assert tok.cpu().reshape(-1).tolist() == c["tokens"]
+
+
+def test_draws_then_presort_end_to_end(h2_golden):
+    """Host draws (bit-exact PCG64) -> device presort == reference assignment."""
+    for d in h2_golden["draws"]:
+        samples = generate_corpus(LengthDistribution(), d["n"], d["seed"])
+        st = stratify(samples, d["bounds"])
+        al = allocate_counts(st.probs, d["lb"])
+        assert list(al.counts) == d["counts"]
+        for step, expect in enumerate(d["batches"]):
+            if isinstance(expect, dict):
+                with pytest.raises(ValueError) as ei:
+                    draw_batch(st, al, seed=1000 + step)
+                assert str(ei.value) == expect["error"]
+                break
+            assert [s.id for s in draw_batch(st, al, seed=1000 + step)] == expect
+    with pytest.raises(ValueError):
+        StratumAllocation((1, 1), 3)

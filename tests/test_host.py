@@ -1,0 +1,142 @@
+"""CPU-only checks: the C-ABI library, host-side logic and validation (no GPU).
+
+The compute paths themselves are covered by the -m gpu suites; here we pin
+what runs on the host (allocate_counts, draw_batch, corpus generation, the
+reference's validation errors) and that the library exports every symbol
+include/b2ddp.h declares.
+"""
+
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2402_02447_b200 as B
+from paper_2402_02447_b200 import _lib
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def header_symbols():
+    text = (ROOT / "include" / "b2ddp.h").read_text()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\*?\s+\*?(b2_\w+)\(", text, re.M)))
+
+
+def test_library_exports_header_symbols():
+    lib = _lib.load(require_device=False)
+    syms = header_symbols()
+    assert len(syms) == 9, syms
+    for s in syms:
+        assert hasattr(lib, s), s
+        assert s in _lib.SIGNATURES, s
+    assert lib.b2_version().decode().startswith("b2ddp")
+    assert lib.b2_clip_workspace_bytes() > 0
+
+
+def test_library_is_sm100a():
+    import subprocess
+
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
+
+
+def test_argument_errors_without_device():
+    """Validation in the C-ABI runs before any device work (returns B2_ERR_*)."""
+    lib = _lib.load(require_device=False)
+    rc = lib.b2_presort_deal(None, None, 1, 10, 3, 1, 512, 10, None, None, None, None, None)
+    assert rc == _lib.B2_ERR_INDIVISIBLE
+    assert "do not divide over 3 GPUs" in lib.b2_last_error().decode()
+    rc = lib.b2_strata_partition(None, None, 1, None, 4, None, None, None, None, 0, None)
+    assert rc == _lib.B2_ERR_INVALID
+    rc = lib.b2_weighted_mean(None, 0, 1, 1, 1, None, None, 1, None, 0, None)
+    assert rc == _lib.B2_ERR_INVALID
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_no_cpu_fallback():
+    with pytest.raises(_lib.B2Error, match="no CPU fallback"):
+        B.sync_bucketwise(B.GradientState(np.ones((1, 4)), ((0, 4),)), B.ClipConfig(1.0, "bucket_wise"))
+    with pytest.raises(_lib.B2Error):
+        B.stratify([B.Sample(0, 5)])
+
+
+def test_config_validation():
+    with pytest.raises(ValueError):
+        B.ClipConfig(0.0, "after_allreduce")
+    with pytest.raises(ValueError):
+        B.ClipConfig(float("inf"), "after_allreduce")
+    with pytest.raises(ValueError):
+        B.ClipConfig(1.0, "sideways")
+    assert B.ClipConfig(2.0, "bucket_wise").mode is B.ClipMode.BUCKET_WISE
+
+
+def test_bucket_layouts():
+    assert B.equal_bucket_layout(7, 3) == ((0, 2), (2, 4), (4, 7))
+    assert B.equal_bucket_layout(10, 3) == ((0, 3), (3, 6), (6, 10))
+    assert B.equal_bucket_layout(4, 4) == ((0, 1), (1, 2), (2, 3), (3, 4))
+    with pytest.raises(ValueError):
+        B.equal_bucket_layout(3, 4)
+    with pytest.raises(ValueError):
+        B.equal_bucket_layout(3, 0)
+    from paper_2402_02447_b200 import synthetic
+
+    base = synthetic.bert_layout(synthetic.BERT_BASE_DIM)
+    large = synthetic.bert_layout(synthetic.BERT_LARGE_DIM)
+    assert len(base) == 17 and base[-1][1] - base[-1][0] == 4_624_640
+    assert len(large) == 52 and large[-1][1] - large[-1][0] == 908_288
+
+
+def test_types_validation():
+    with pytest.raises(ValueError):
+        B.Sample(-1, 5)
+    with pytest.raises(ValueError):
+        B.Sample(0, 0)
+    with pytest.raises(ValueError):
+        B.Topology(0, 8)
+    assert B.Topology(2, 4).total_gpus == 8
+    with pytest.raises(ValueError):
+        B.LengthDistribution(bin_probs=(0.5, 0.5, 0.5, 0.5))
+    with pytest.raises(ValueError):
+        B.StratumAllocation((1, 1), 3)
+
+
+def test_host_generation_matches_reference(h2_golden):
+    for c in h2_golden["corpora"]:
+        s = B.generate_corpus(B.LengthDistribution(), c["n"], c["seed"])
+        assert [x.length for x in s] == c["lengths"]
+
+
+def test_allocate_counts_golden(h2_golden):
+    for a in h2_golden["allocate"]:
+        assert list(B.allocate_counts(a["probs"], a["lb"]).counts) == a["counts"]
+    assert B.allocate_counts((5 / 16, 2 / 16, 3 / 16, 6 / 16), 16).counts == (5, 2, 3, 6)
+    assert B.allocate_counts((0.373, 0.197, 0.117, 0.314), 16).counts == (6, 3, 2, 5)
+    assert B.allocate_counts((0.5, 0.5), 3).counts == (2, 1)
+    assert B.allocate_counts((0.3, 0.7), 0).counts == (0, 0)
+    with pytest.raises(ValueError, match="negative"):
+        B.allocate_counts((0.5, -0.1, 0.6), 8)
+    with pytest.raises(ValueError):
+        B.allocate_counts((0.0, 0.0), 8)
+
+
+def test_draw_batch_golden(h2_golden):
+    """Host draws reproduce the reference's PCG64 draw sequence and errors exactly."""
+    from oracle import ddp_oracle as O
+
+    for d in h2_golden["draws"]:
+        lens = B.seqdata.generate_lengths(B.LengthDistribution(), d["n"], d["seed"])
+        pools, probs = O.stratify(lens, d["bounds"])  # strata built by the oracle (no GPU here)
+        samples = [B.Sample(i, int(x)) for i, x in enumerate(lens)]
+        st = B.strata.Strata(tuple(d["bounds"]), [[samples[i] for i in p] for p in pools], probs)
+        al = B.allocate_counts(st.probs, d["lb"])
+        for step, expect in enumerate(d["batches"]):
+            if isinstance(expect, dict):
+                with pytest.raises(ValueError) as ei:
+                    B.draw_batch(st, al, seed=1000 + step)
+                assert str(ei.value) == expect["error"]
+                break
+            assert [s.id for s in B.draw_batch(st, al, seed=1000 + step)] == expect
