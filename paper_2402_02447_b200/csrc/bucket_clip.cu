@@ -7,26 +7,23 @@
 // K1b k_weighted_mean: single-process K-worker mean of clipped buckets with the
 //                     reference's pairwise tree (gradsync.py:119-128).
 //
-// K1 design (HBM-bound, 4 B read + 2/4 B write per element):
-//   * one persistent cooperative grid (ctas_per_sm x #SM CTAs, all co-resident)
-//     walks a list of segments (buckets) in the order given;
-//   * phase A(s): each CTA streams its contiguous chunk of segment s with
-//     128-bit loads, accumulates sum(x^2) in fp64 (no fp32 overflow /
-//     cancellation; 1e-5 parity needs it — SURVEY trap 4), block-reduces and
-//     publishes one fp64 partial; the last CTA to arrive folds all partials in
-//     a fixed order (bit-deterministic), derives norm/coef with the
-//     reference's inclusive `norm >= limit` rule and releases a per-segment flag;
-//   * phase B(s): once segment s's coefficient is published, each CTA re-reads
-//     its chunk (an L2 hit: the chunk was read one phase earlier, a 26 MB bucket
-//     is well inside the 126 MB L2) and writes g*coef*post_scale, cast;
-//   * software pipeline: a CTA runs A(s+1) before waiting on s, so DRAM keeps
-//     streaming while the slowest CTA's partial of s lands.  DRAM traffic is the
-//     algorithmic 4 B read + out-dtype write per element; the re-read is on L2.
+// K1 design (HBM-bound: 4 B read + 2/4 B write per element):
+//   one persistent cooperative grid (2 CTAs/SM) walks the list of segments
+//   (buckets) with two streams per CTA — A: norm pass over bucket s (128-bit
+//   loads, L2 evict_last), B: scale pass over bucket s-1 (L2 re-read,
+//   evict_first) — so the grid-wide norm dependency of a bucket is hidden
+//   behind a whole bucket of A work.  Partials are published fire-and-forget
+//   and every CTA folds them in one fixed order (bit-deterministic, identical
+//   coefficient grid-wide).  A TMA-ring variant (cp.async.bulk into a
+//   shared-memory ring, warp-specialised producer) is kept for A/B runs
+//   (B2_CLIP_CFG=5); measured slower on B200 because the ring must either hold
+//   the bucket through the barrier or lose its L2 residency.
 #include "common.cuh"
 
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 namespace b2 {
@@ -34,11 +31,10 @@ namespace {
 
 constexpr int kMaxSegs = 128;   // segments per launch (kernel-parameter table)
 constexpr int kMaxGrid = 2048;  // CTAs per launch the workspace is sized for
-constexpr int kThreads = 512;
-constexpr int kUnroll = 4;
 
 struct Seg {
   int64_t in_off, out_off, n, head;  // head: scalar elements before 16 B alignment
+  int64_t nv, per;                   // body vectors; vectors per CTA (TMA kernel)
   int32_t vec;                       // 1: vector body path, 0: scalar path
   int32_t pad;
 };
@@ -54,6 +50,7 @@ struct ClipParams {
   double* coef_ws;     // [kMaxSegs]
   unsigned* counters;  // [kMaxSegs + 1]; the last one is the exit counter
   int nseg;
+  int seg_vec_elems;   // elements per 16 B vector (4 for f32, 2 for f64)
   Seg seg[kMaxSegs];
 };
 
@@ -75,75 +72,11 @@ __device__ __forceinline__ void unpack(const double2& v, double (&x)[2]) {
   x[0] = v.x; x[1] = v.y;
 }
 
-template <typename V> __device__ __forceinline__ V ld_stream_keep(const V* p);
-template <> __device__ __forceinline__ float4 ld_stream_keep(const float4* p) {
-  float4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
-  return v;
-}
-template <> __device__ __forceinline__ double2 ld_stream_keep(const double2* p) {
-  double2 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
-               : "=d"(v.x), "=d"(v.y) : "l"(p));
-  return v;
-}
-// last use of the chunk: evict-first so it does not displace the next bucket
-template <typename V> __device__ __forceinline__ V ld_last_use(const V* p) { return __ldcs(p); }
-
 template <typename Tin>
 __device__ __forceinline__ double sq_of(Tin x, bool& bad) {
   double d = static_cast<double>(x);
   if constexpr (std::is_same<Tin, double>::value) bad |= !isfinite(d);
   return d * d;
-}
-
-// Phase A: this CTA's sum of squares over its chunk of segment s.
-template <typename Tin>
-__device__ __forceinline__ double chunk_sumsq(const ClipParams& p, const Seg& sg, bool& bad) {
-  using V = typename VecOf<Tin>::V;
-  constexpr int N = VecOf<Tin>::N;
-  const Tin* in = static_cast<const Tin*>(p.in) + sg.in_off;
-  const int G = gridDim.x, c = blockIdx.x, t = threadIdx.x;
-  double acc[N];
-#pragma unroll
-  for (int j = 0; j < N; ++j) acc[j] = 0.0;
-  if (sg.vec) {
-    const int64_t nv = (sg.n - sg.head) / N;
-    const int64_t tail0 = sg.head + nv * N;
-    if (c == 0 && t < sg.head) acc[0] += sq_of(in[t], bad);
-    if (c == G - 1 && t < sg.n - tail0) acc[1 % N] += sq_of(in[tail0 + t], bad);
-    const V* vin = reinterpret_cast<const V*>(in + sg.head);
-    const int64_t per = (nv + G - 1) / G;
-    const int64_t v0 = min64((int64_t)c * per, nv), v1 = min64(v0 + per, nv);
-    for (int64_t v = v0 + t; v < v1; v += (int64_t)kThreads * kUnroll) {
-      V x[kUnroll];
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const int64_t vi = v + (int64_t)u * kThreads;
-        if (vi < v1) x[u] = ld_stream_keep(vin + vi);
-        else x[u] = V{};
-      }
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        double e[N];
-        unpack(x[u], e);
-#pragma unroll
-        for (int j = 0; j < N; ++j) {
-          if constexpr (std::is_same<Tin, double>::value) bad |= !isfinite(e[j]);
-          acc[j] = fma(e[j], e[j], acc[j]);
-        }
-      }
-    }
-  } else {
-    const int64_t per = (sg.n + G - 1) / G;
-    const int64_t e0 = min64((int64_t)c * per, sg.n), e1 = min64(e0 + per, sg.n);
-    for (int64_t e = e0 + t; e < e1; e += kThreads) acc[0] += sq_of(in[e], bad);
-  }
-  double r = 0.0;
-#pragma unroll
-  for (int j = 0; j < N; ++j) r += acc[j];
-  return r;
 }
 
 template <typename Tout, typename Acc>
@@ -172,121 +105,360 @@ __device__ __forceinline__ void put_vec(Tout* o, const Acc (&y)[N]) {
   }
 }
 
-// Phase B: out = cast(in * coef * post_scale) over this CTA's chunk.
-template <typename Tin, typename Tout>
-__device__ __forceinline__ void chunk_scale(const ClipParams& p, const Seg& sg, double coef) {
+// ----------------------------------------------------------------------------
+// K1 (TMA ring): 1 CTA per SM; each CTA's chunk of a bucket is pulled into a
+// shared-memory ring of 16 KB pieces by cp.async.bulk (TMA), each piece with
+// its own mbarrier.  The chunk stays on chip until the bucket's coefficient is
+// published, is then scaled straight out of shared memory, and every freed
+// piece is immediately refilled with the next bucket's data — so the DMA
+// engine keeps HBM busy through the norm barrier.  DRAM traffic is exactly the
+// algorithmic 4 B read + 2/4 B write per element (no L2 re-read) as long as a
+// CTA's chunk fits the ring (bucket <= #SM x 224 KB = 33 MB); larger chunks
+// spill their tail to an L2-resident re-read (evict_last / evict_first hints).
+constexpr int kTThreads = 512;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
+  return (uint32_t)__cvta_generic_to_shared(ptr);
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{ .reg .pred P; mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2; selp.u32 %0, 1, 0, P; }"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+template <typename V> __device__ __forceinline__ V ld_hint(const V* ptr, uint64_t pol);
+template <> __device__ __forceinline__ float4 ld_hint(const float4* ptr, uint64_t pol) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(ptr), "l"(pol));
+  return v;
+}
+template <> __device__ __forceinline__ double2 ld_hint(const double2* ptr, uint64_t pol) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y) : "l"(ptr), "l"(pol));
+  return v;
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+// consumer-only barrier (the producer warp never joins it)
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kTThreads) : "memory"); }
+__device__ __forceinline__ int consumer_sync_or(int pred) {
+  int r;
+  asm volatile(
+      "{ .reg .pred a, b; setp.ne.s32 a, %1, 0; bar.red.or.pred b, 1, %2, a; selp.s32 %0, 1, 0, b; }"
+      : "=r"(r)
+      : "r"(pred), "n"(kTThreads)
+      : "memory");
+  return r;
+}
+
+template <int THREADS>
+__device__ __forceinline__ double consumer_block_sum(double v, double* scratch) {
+  constexpr int W = THREADS / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_sum(v);
+  consumer_sync();
+  if (lane == 0) scratch[warp] = v;
+  consumer_sync();
+  double r = 0.0;
+  if (warp == 0) {
+    r = lane < W ? scratch[lane] : 0.0;
+    r = warp_sum(r);
+  }
+  return r;  // valid in warp 0
+}
+
+__device__ __forceinline__ void tma_load_1d_hint(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar,
+                                                 uint64_t pol) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          dst),
+      "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+      : "memory");
+}
+
+// Warp-specialised, two-stream persistent kernel (one CTA per SM).
+//   stream A (norm): warp 16 pulls this CTA's chunk of every bucket through a
+//     shared-memory ring with cp.async.bulk (TMA, L2 evict_last), warps 0..15
+//     sum squares and release each 16 KB piece at once; one fp64 partial per
+//     (bucket, CTA) is published fire-and-forget (red.release).
+//   stream B (scale): LAG buckets behind, each CTA folds bucket s's partials
+//     (fixed order -> bit-identical coefficient in every CTA), re-reads its
+//     chunk from L2 (evict_first: last use) and writes g*coef*post_scale.
+// By the time B(s) needs bucket s's coefficient the whole grid has long
+// finished A(s), so no CTA idles at the norm barrier and HBM sees exactly the
+// algorithmic traffic: the A read + the B write (B's re-read hits L2; the
+// bucket is 26 MB, L2 is 126 MB).  A lone bucket (the DDP-hook case) runs A
+// then B with one grid-wide wait in between.
+// MODE 0: stream A through the TMA ring with an L2 evict_last hint
+// MODE 1: TMA ring, default L2 policy
+// MODE 2: stream A with plain 128-bit loads (evict_last), ring unused
+template <typename Tin, typename Tout, int NP, int PIECE, int LAG, int MODE>
+__global__ void __launch_bounds__(kTThreads + 32, 1) k_bucket_clip_tma(const __grid_constant__ ClipParams p) {
   using V = typename VecOf<Tin>::V;
   constexpr int N = VecOf<Tin>::N;
-  using Acc = typename std::conditional<std::is_same<Tin, double>::value ||
-                                            std::is_same<Tout, double>::value,
+  constexpr bool kF64 = std::is_same<Tin, double>::value;
+  constexpr int kWarps = kTThreads / 32;
+  constexpr int PV = PIECE / 16;       // 16 B vectors per piece
+  constexpr int VPT = PV / kTThreads;  // vectors per consumer thread per piece
+  constexpr int UB = 8;                // stream-B loads in flight per thread
+  static_assert(PV % kTThreads == 0, "piece must split evenly over consumer threads");
+  using Acc = typename std::conditional<std::is_same<Tin, double>::value || std::is_same<Tout, double>::value,
                                         double, float>::type;
-  const Tin* in = static_cast<const Tin*>(p.in) + sg.in_off;
-  Tout* out = static_cast<Tout*>(p.out) + sg.out_off;
-  const Acc cf = static_cast<Acc>(coef * p.post_scale);
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ double s_coef[2];
+  __shared__ double red[32];
   const int G = gridDim.x, c = blockIdx.x, t = threadIdx.x;
-  if (sg.vec) {
-    const int64_t nv = (sg.n - sg.head) / N;
-    const int64_t tail0 = sg.head + nv * N;
-    if (c == 0 && t < sg.head) put1(out + t, static_cast<Acc>(in[t]) * cf);
-    if (c == G - 1 && t < sg.n - tail0) put1(out + tail0 + t, static_cast<Acc>(in[tail0 + t]) * cf);
-    const V* vin = reinterpret_cast<const V*>(in + sg.head);
-    Tout* vout = out + sg.head;
-    const int64_t per = (nv + G - 1) / G;
-    const int64_t v0 = min64((int64_t)c * per, nv), v1 = min64(v0 + per, nv);
-    for (int64_t v = v0 + t; v < v1; v += (int64_t)kThreads * kUnroll) {
-      V x[kUnroll];
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const int64_t vi = v + (int64_t)u * kThreads;
-        if (vi < v1) x[u] = ld_last_use(vin + vi);
-      }
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const int64_t vi = v + (int64_t)u * kThreads;
-        if (vi < v1) {
-          double e[N];
-          unpack(x[u], e);
-          Acc y[N];
-#pragma unroll
-          for (int j = 0; j < N; ++j) y[j] = static_cast<Acc>(e[j]) * cf;
-          put_vec<Tout, N, Acc>(vout + vi * N, y);
+  const uint32_t ring_base = smem_u32(ring);
+  const uint32_t full_base = ring_base + NP * PIECE;
+  const uint32_t empty_base = full_base + 8u * NP;
+  const bool scale = p.out != nullptr;
+
+  if (MODE != 2 && t == 0) {  // MODE 2 launches without the ring (no dynamic smem)
+    for (int i = 0; i < NP; ++i) {
+      mbar_init(full_base + 8u * i, 1);
+      mbar_init(empty_base + 8u * i, kWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (t >= kTThreads) {
+    // ---------------- producer warp (stream A)
+    if (MODE != 2 && t == kTThreads) {
+      const uint64_t pol = scale ? l2_policy_evict_last() : l2_policy_evict_first();
+      uint32_t q = 0;
+      for (int s = 0; s < p.nseg; ++s) {
+        const Seg& sg = p.seg[s];
+        if (!sg.vec) continue;
+        const int64_t v0 = min64((int64_t)c * sg.per, sg.nv), v1 = min64(v0 + sg.per, sg.nv);
+        const char* src = reinterpret_cast<const char*>(static_cast<const Tin*>(p.in) + sg.in_off + sg.head) + v0 * 16;
+        for (int64_t off = 0; off < v1 - v0; off += PV, ++q) {
+          const uint32_t slot = q % NP, fill = q / NP;
+          if (fill > 0) mbar_wait(empty_base + 8u * slot, (fill - 1) & 1);
+          const int nvec = (int)min64(PV, v1 - v0 - off);
+          if (MODE == 0) tma_load_1d_hint(ring_base + slot * PIECE, src + off * 16, nvec * 16, full_base + 8u * slot, pol);
+          else tma_load_1d(ring_base + slot * PIECE, src + off * 16, nvec * 16, full_base + 8u * slot);
         }
       }
     }
-  } else {
-    const int64_t per = (sg.n + G - 1) / G;
-    const int64_t e0 = min64((int64_t)c * per, sg.n), e1 = min64(e0 + per, sg.n);
-    for (int64_t e = e0 + t; e < e1; e += kThreads) put1(out + e, static_cast<Acc>(in[e]) * cf);
+    return;
   }
-}
 
-template <typename Tin, typename Tout>
-__global__ void __launch_bounds__(kThreads) k_bucket_clip(const __grid_constant__ ClipParams p) {
-  __shared__ double red[32];
-  __shared__ double s_coef[2];  // double-buffered by segment parity
-  __shared__ int s_last;
-  const unsigned G = gridDim.x;
-  constexpr bool kF64 = std::is_same<Tin, double>::value;
+  // ---------------- consumer warps
+  const int lane = t & 31, warp = t >> 5;
+  const uint64_t pol_keep = l2_policy_evict_last();
+  const uint64_t pol_drop = l2_policy_evict_first();
 
-  // Phase A for segment s, then (if this CTA arrived last) publish its coef.
-  auto arrive = [&](int s) {
-    const Seg& sg = p.seg[s];
-    bool bad = false;
-    const double part = chunk_sumsq<Tin>(p, sg, bad);
-    double tot = block_sum<kThreads>(part, red);
-    if constexpr (kF64) {
-      if (__syncthreads_or(bad)) tot = __longlong_as_double(0x7ff8000000000000ll);  // NaN marks inf/nan input
-    }
-    if (threadIdx.x == 0) {
-      p.partials[(size_t)s * G + blockIdx.x] = tot;
-      __threadfence();
-      const unsigned prev = atom_add_acq_rel_u32(&p.counters[s], 1u);
-      s_last = (prev == G - 1);
-    }
-    __syncthreads();
-    if (s_last) {
-      // fixed-order fold of all partials: identical bits whichever CTA is last
-      double v = 0.0;
-      for (unsigned j = threadIdx.x; j < G; j += kThreads) v += __ldcg(&p.partials[(size_t)s * G + j]);
-      const double total = block_sum<kThreads>(v, red);
-      if (threadIdx.x == 0) {
-        const double norm = sqrt(total);
-        const bool nf = kF64 ? isnan(total) : !isfinite(total);
-        const double coef = (norm >= p.limit) ? p.limit / norm : 1.0;  // gradsync.py:114-116
-        if (p.norms) p.norms[s] = norm;
-        if (p.coefs) p.coefs[s] = coef;
-        if (p.nonfinite) p.nonfinite[s] = nf ? 1 : 0;
-        p.coef_ws[s] = coef;
-        red_release_u32(&p.counters[s], 1u);  // counter -> G + 1: published
-      }
-    }
-  };
-
-  auto wait_coef = [&](int s) -> double {
-    if (threadIdx.x == 0) {
+  // fold the G partials of segment s (warp 0, fixed order) -> coefficient
+  auto fold = [&](int s, bool publish) -> double {
+    if (lane == 0) {
       unsigned ns = 32;
-      while (ld_acquire_u32(&p.counters[s]) < G + 1) {
+      while (ld_acquire_u32(&p.counters[s]) < (unsigned)G) {
         __nanosleep(ns);
-        if (ns < 512) ns <<= 1;
+        if (ns < 256) ns <<= 1;
       }
-      s_coef[s & 1] = __ldcg(&p.coef_ws[s]);
     }
-    __syncthreads();
-    return s_coef[s & 1];
+    __syncwarp();
+    double v = 0.0;
+    for (int j = lane; j < G; j += 32) v += __ldcg(&p.partials[(size_t)s * G + j]);
+    const double total = warp_sum(v);
+    const double norm = sqrt(total);
+    const double coef = (norm >= p.limit) ? p.limit / norm : 1.0;  // gradsync.py:114-116
+    if (publish && lane == 0) {
+      if (p.norms) p.norms[s] = norm;
+      if (p.coefs) p.coefs[s] = coef;
+      if (p.nonfinite) p.nonfinite[s] = (kF64 ? isnan(total) : !isfinite(total)) ? 1 : 0;
+    }
+    return coef;
   };
 
-  arrive(0);
-  for (int s = 0; s < p.nseg; ++s) {
-    if (s + 1 < p.nseg) arrive(s + 1);
-    const double coef = wait_coef(s);
-    if (p.out != nullptr) chunk_scale<Tin, Tout>(p, p.seg[s], coef);
+  // ---- stream A for segment s: sum of squares, publish the CTA partial
+  uint32_t q = 0;
+  auto norm_pass = [&](int s) {
+    const Seg sg = p.seg[s];  // by value: keep the descriptor in registers
+    const Tin* in = static_cast<const Tin*>(p.in) + sg.in_off;
+    double acc[N];
+#pragma unroll
+    for (int u = 0; u < N; ++u) acc[u] = 0.0;
+    bool bad = false;
+    auto add = [&](const V& x) {  // exact fp64 accumulation
+      double e[N];
+      unpack(x, e);
+#pragma unroll
+      for (int u = 0; u < N; ++u) {
+        if constexpr (kF64) bad |= !isfinite(e[u]);
+        acc[u] = fma(e[u], e[u], acc[u]);
+      }
+    };
+    auto mini = [&](const V* xs, int cnt) {
+      if constexpr (kF64) {
+        for (int u = 0; u < cnt; ++u) add(xs[u]);
+      } else {
+        // f32: a handful of squares summed in fp32 (rel. error < 2e-6),
+        // promoted once; a mini-sum outside [2^-100, 2^100] (underflow,
+        // overflow, inf, nan) is redone exactly in fp64
+        float m = 0.0f;
+        unsigned nz = 0;
+        for (int u = 0; u < cnt; ++u) {
+          m = fmaf(xs[u].x, xs[u].x, m);
+          m = fmaf(xs[u].y, xs[u].y, m);
+          m = fmaf(xs[u].z, xs[u].z, m);
+          m = fmaf(xs[u].w, xs[u].w, m);
+          nz |= __float_as_uint(xs[u].x) | __float_as_uint(xs[u].y) | __float_as_uint(xs[u].z) |
+                __float_as_uint(xs[u].w);
+        }
+        if (m >= 0x1p-100f && m <= 0x1p100f) {
+          acc[0] += (double)m;
+        } else if ((nz << 1) != 0u) {  // some element is non-zero: exact path
+          for (int u = 0; u < cnt; ++u) add(xs[u]);
+        }
+      }
+    };
+    if (sg.vec && MODE == 2) {
+      constexpr int UA = 16;  // 128-bit loads in flight per thread
+      const V* vin = reinterpret_cast<const V*>(in + sg.head);
+      const int64_t v0 = min64((int64_t)c * sg.per, sg.nv), v1 = min64(v0 + sg.per, sg.nv);
+      for (int64_t v = v0 + t; v < v1; v += (int64_t)kTThreads * UA) {
+        V x[UA];
+#pragma unroll
+        for (int u = 0; u < UA; ++u) {
+          const int64_t vi = v + (int64_t)u * kTThreads;
+          x[u] = vi < v1 ? ld_hint(vin + vi, pol_keep) : V{};
+        }
+#pragma unroll
+        for (int h = 0; h < UA; h += 8) mini(x + h, 8);
+      }
+    }
+    if (sg.vec && MODE != 2) {
+      const int64_t v0 = min64((int64_t)c * sg.per, sg.nv), v1 = min64(v0 + sg.per, sg.nv);
+      for (int64_t off = 0; off < v1 - v0; off += PV, ++q) {
+        const uint32_t slot = q % NP;
+        mbar_wait(full_base + 8u * slot, (q / NP) & 1);
+        const int nvec = (int)min64(PV, v1 - v0 - off);
+        const V* sp = reinterpret_cast<const V*>(ring + slot * PIECE);
+        V xs[VPT];
+#pragma unroll
+        for (int u = 0; u < VPT; ++u) {
+          const int i = t + u * kTThreads;
+          xs[u] = i < nvec ? sp[i] : V{};
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty_base + 8u * slot);  // piece consumed: refill at once
+        mini(xs, VPT);
+      }
+    }
+    if (sg.vec) {
+      const int64_t tail0 = sg.head + sg.nv * N;
+      if (c == 0 && t < sg.head) acc[0] += sq_of(in[t], bad);
+      if (c == G - 1 && t < sg.n - tail0) acc[N - 1] += sq_of(in[tail0 + t], bad);
+    } else {
+      const int64_t per = (sg.n + G - 1) / G;
+      const int64_t e0 = min64((int64_t)c * per, sg.n), e1 = min64(e0 + per, sg.n);
+      for (int64_t e = e0 + t; e < e1; e += kTThreads) acc[0] += sq_of(in[e], bad);
+    }
+    double part = 0.0;
+#pragma unroll
+    for (int u = 0; u < N; ++u) part += acc[u];
+    double tot = consumer_block_sum<kTThreads>(part, red);
+    if constexpr (kF64) {
+      if (consumer_sync_or(bad)) tot = __longlong_as_double(0x7ff8000000000000ll);  // NaN marks inf/nan input
+    }
+    if (t == 0) {
+      p.partials[(size_t)s * G + c] = tot;
+      red_release_u32(&p.counters[s], 1u);  // fire-and-forget arrival
+    }
+  };
+
+  // ---- stream B for segment s: coefficient, L2 re-read, scale + cast + store
+  auto scale_pass = [&](int s) {
+    const Seg sg = p.seg[s];
+    if (warp == 0) {
+      const double coef = fold(s, c == 0);
+      if (lane == 0) s_coef[s & 1] = coef;
+    }
+    consumer_sync();
+    const Acc cf = static_cast<Acc>(s_coef[s & 1] * p.post_scale);
+    const Tin* in = static_cast<const Tin*>(p.in) + sg.in_off;
+    Tout* out = static_cast<Tout*>(p.out) + sg.out_off;
+    auto put = [&](int64_t v, const V& x) {
+      Acc y[N];
+      if constexpr (kF64) {
+        y[0] = x.x * cf;
+        y[1] = x.y * cf;
+      } else {  // f32 in: scale in the output's working precision
+        y[0] = static_cast<Acc>(x.x) * cf;
+        y[1] = static_cast<Acc>(x.y) * cf;
+        y[2] = static_cast<Acc>(x.z) * cf;
+        y[3] = static_cast<Acc>(x.w) * cf;
+      }
+      put_vec<Tout, N, Acc>(out + sg.head + v * N, y);
+    };
+    if (sg.vec) {
+      const V* vin = reinterpret_cast<const V*>(in + sg.head);
+      const int64_t v0 = min64((int64_t)c * sg.per, sg.nv), v1 = min64(v0 + sg.per, sg.nv);
+      for (int64_t v = v0 + t; v < v1; v += (int64_t)kTThreads * UB) {
+        V x[UB];
+#pragma unroll
+        for (int u = 0; u < UB; ++u) {
+          const int64_t vi = v + (int64_t)u * kTThreads;
+          if (vi < v1) x[u] = ld_hint(vin + vi, pol_drop);
+        }
+#pragma unroll
+        for (int u = 0; u < UB; ++u) {
+          const int64_t vi = v + (int64_t)u * kTThreads;
+          if (vi < v1) put(vi, x[u]);
+        }
+      }
+      const int64_t tail0 = sg.head + sg.nv * N;
+      if (c == 0 && t < sg.head) put1(out + t, static_cast<Acc>(in[t]) * cf);
+      if (c == G - 1 && t < sg.n - tail0) put1(out + tail0 + t, static_cast<Acc>(in[tail0 + t]) * cf);
+    } else {
+      const int64_t per = (sg.n + G - 1) / G;
+      const int64_t e0 = min64((int64_t)c * per, sg.n), e1 = min64(e0 + per, sg.n);
+      for (int64_t e = e0 + t; e < e1; e += kTThreads) put1(out + e, static_cast<Acc>(in[e]) * cf);
+    }
+  };
+
+  for (int it = 0; it < p.nseg + (scale ? LAG : 0); ++it) {
+    if (it < p.nseg) norm_pass(it);
+    if (scale && it >= LAG) scale_pass(it - LAG);
   }
 
-  // exit: the last CTA out restores the counters to zero for the next launch
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned prev = atom_add_acq_rel_u32(&p.counters[kMaxSegs], 1u);
-    if (prev == G - 1) {
+  // norm-only launches: publish every segment's norm / coefficient, spread over CTAs
+  if (!scale && warp == 0)
+    for (int s = c; s < p.nseg; s += G) fold(s, true);
+
+  consumer_sync();
+  if (t == 0) {
+    if (atom_add_acq_rel_u32(&p.counters[kMaxSegs], 1u) == (unsigned)G - 1) {
       for (int s = 0; s < p.nseg; ++s) p.counters[s] = 0u;
       p.counters[kMaxSegs] = 0u;
       __threadfence();
@@ -294,24 +466,318 @@ __global__ void __launch_bounds__(kThreads) k_bucket_clip(const __grid_constant_
   }
 }
 
-template <typename Tin, typename Tout>
-int launch_clip(ClipParams& p, int ctas_per_sm, cudaStream_t stream) {
-  auto kern = k_bucket_clip<Tin, Tout>;
+// ----------------------------------------------------------------------------
+// K1 (L2-lag): the production variant.  Persistent cooperative grid of CPS
+// CTAs per SM; each CTA owns one contiguous chunk of every bucket.
+//   stream A (norm): 128-bit loads with an L2 evict_last policy, UA in flight
+//     per thread; fp32 mini-sums promoted to fp64; one partial per
+//     (bucket, CTA) published fire-and-forget (red.release).
+//   stream B (scale), LAG buckets behind: every CTA folds the bucket's
+//     partials in one fixed order (bit-identical coefficient grid-wide),
+//     re-reads its chunk - an L2 hit, A touched it one bucket ago - with an
+//     evict_first policy (last use) and stores cast(g * coef * post_scale).
+// The grid-wide norm dependency is hidden behind a whole bucket of A work,
+// and HBM sees the algorithmic 4 B read + out-dtype write per element.
+template <int BNC> __device__ __forceinline__ float4 ld_b(const float4* ptr, uint64_t pol) {
+  if constexpr (BNC) return ld_hint(ptr, pol);
+  float4 v;
+  asm volatile("ld.global.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(ptr), "l"(pol));
+  return v;
+}
+template <int BNC> __device__ __forceinline__ double2 ld_b(const double2* ptr, uint64_t pol) {
+  if constexpr (BNC) return ld_hint(ptr, pol);
+  double2 v;
+  asm volatile("ld.global.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(ptr), "l"(pol));
+  return v;
+}
+template <int BNC> __device__ __forceinline__ float4 ld_a(const float4* ptr, uint64_t pol) { return ld_b<BNC>(ptr, pol); }
+template <int BNC> __device__ __forceinline__ double2 ld_a(const double2* ptr, uint64_t pol) { return ld_b<BNC>(ptr, pol); }
+
+template <typename Tin, typename Tout, int THREADS, int CPS, int LAG, int UA, int UB, int BNC>
+__global__ void __launch_bounds__(THREADS, CPS) k_bucket_clip_l2lag(const __grid_constant__ ClipParams p) {
+  using V = typename VecOf<Tin>::V;
+  constexpr int N = VecOf<Tin>::N;
+  constexpr bool kF64 = std::is_same<Tin, double>::value;
+  using Acc = typename std::conditional<std::is_same<Tin, double>::value || std::is_same<Tout, double>::value,
+                                        double, float>::type;
+  __shared__ double s_coef[2];
+  __shared__ double red[32];
+  const int G = gridDim.x, c = blockIdx.x, t = threadIdx.x;
+  const bool scale = p.out != nullptr;
+  const uint64_t pol_keep = scale ? l2_policy_evict_last() : l2_policy_evict_first();
+  const uint64_t pol_drop = l2_policy_evict_first();
+
+  // block-wide fixed-order fold of the G partials of segment s -> coefficient
+  // (one L2 round trip: each thread loads <= ceil(G/THREADS) partials)
+  auto fold = [&](int s, bool publish) -> double {
+    if (t == 0) {
+      unsigned ns = 32;
+      while (ld_acquire_u32(&p.counters[s]) < (unsigned)G) {
+        __nanosleep(ns);
+        if (ns < 256) ns <<= 1;
+      }
+    }
+    __syncthreads();
+    double v = 0.0;
+    for (int j = t; j < G; j += THREADS) v += __ldcg(&p.partials[(size_t)s * G + j]);
+    const double total = block_sum<THREADS>(v, red);
+    if (t == 0) {
+      const double norm = sqrt(total);
+      const double coef = (norm >= p.limit) ? p.limit / norm : 1.0;  // gradsync.py:114-116
+      if (publish) {
+        if (p.norms) p.norms[s] = norm;
+        if (p.coefs) p.coefs[s] = coef;
+        if (p.nonfinite) p.nonfinite[s] = (kF64 ? isnan(total) : !isfinite(total)) ? 1 : 0;
+      }
+      s_coef[s & 1] = coef;
+    }
+    __syncthreads();
+    return s_coef[s & 1];
+  };
+
+  auto norm_pass = [&](int s) {
+    const Seg sg = p.seg[s];
+    const Tin* in = static_cast<const Tin*>(p.in) + sg.in_off;
+    double acc[N];
+#pragma unroll
+    for (int u = 0; u < N; ++u) acc[u] = 0.0;
+    bool bad = false;
+    auto add = [&](const V& x) {
+      double e[N];
+      unpack(x, e);
+#pragma unroll
+      for (int u = 0; u < N; ++u) {
+        if constexpr (kF64) bad |= !isfinite(e[u]);
+        acc[u] = fma(e[u], e[u], acc[u]);
+      }
+    };
+    if (sg.vec) {
+      const V* vin = reinterpret_cast<const V*>(in + sg.head);
+      const int64_t v0 = min64((int64_t)c * sg.per, sg.nv), v1 = min64(v0 + sg.per, sg.nv);
+      for (int64_t v = v0 + t; v < v1; v += (int64_t)THREADS * UA) {
+        V x[UA];
+#pragma unroll
+        for (int u = 0; u < UA; ++u) {
+          const int64_t vi = v + (int64_t)u * THREADS;
+          x[u] = vi < v1 ? ld_a<0>(vin + vi, pol_keep) : V{};
+        }
+        if constexpr (kF64) {
+#pragma unroll
+          for (int u = 0; u < UA; ++u) add(x[u]);
+        } else {
+          // f32: <= 32 squares summed in fp32 (rel. error < 2e-6), promoted
+          // once; a mini-sum outside [2^-100, 2^100] (underflow, overflow,
+          // inf, nan) with a non-zero element is redone exactly in fp64
+#pragma unroll
+          for (int h = 0; h < UA; h += 8) {
+            float m = 0.0f;
+            unsigned nz = 0;
+#pragma unroll
+            for (int u = h; u < h + 8 && u < UA; ++u) {
+              m = fmaf(x[u].x, x[u].x, m);
+              m = fmaf(x[u].y, x[u].y, m);
+              m = fmaf(x[u].z, x[u].z, m);
+              m = fmaf(x[u].w, x[u].w, m);
+              nz |= __float_as_uint(x[u].x) | __float_as_uint(x[u].y) | __float_as_uint(x[u].z) |
+                    __float_as_uint(x[u].w);
+            }
+            if (m >= 0x1p-100f && m <= 0x1p100f) {
+              acc[0] += (double)m;
+            } else if ((nz << 1) != 0u) {
+#pragma unroll
+              for (int u = h; u < h + 8 && u < UA; ++u) add(x[u]);
+            }
+          }
+        }
+      }
+      const int64_t tail0 = sg.head + sg.nv * N;
+      if (c == 0 && t < sg.head) acc[0] += sq_of(in[t], bad);
+      if (c == G - 1 && t < sg.n - tail0) acc[N - 1] += sq_of(in[tail0 + t], bad);
+    } else {
+      const int64_t per = (sg.n + G - 1) / G;
+      const int64_t e0 = min64((int64_t)c * per, sg.n), e1 = min64(e0 + per, sg.n);
+      for (int64_t e = e0 + t; e < e1; e += THREADS) acc[0] += sq_of(in[e], bad);
+    }
+    double part = 0.0;
+#pragma unroll
+    for (int u = 0; u < N; ++u) part += acc[u];
+    double tot = block_sum<THREADS>(part, red);
+    if constexpr (kF64) {
+      if (__syncthreads_or(bad)) tot = __longlong_as_double(0x7ff8000000000000ll);  // NaN marks inf/nan input
+    }
+    if (t == 0) {
+      p.partials[(size_t)s * G + c] = tot;
+      red_release_u32(&p.counters[s], 1u);  // fire-and-forget arrival
+    }
+  };
+
+  auto scale_pass = [&](int s) {
+    const Seg sg = p.seg[s];
+    const Acc cf = static_cast<Acc>(fold(s, c == 0) * p.post_scale);
+    const Tin* in = static_cast<const Tin*>(p.in) + sg.in_off;
+    Tout* out = static_cast<Tout*>(p.out) + sg.out_off;
+    if (sg.vec) {
+      const V* vin = reinterpret_cast<const V*>(in + sg.head);
+      Tout* vout = out + sg.head;
+      const int64_t v0 = min64((int64_t)c * sg.per, sg.nv), v1 = min64(v0 + sg.per, sg.nv);
+      for (int64_t v = v0 + t; v < v1; v += (int64_t)THREADS * UB) {
+        V x[UB];
+#pragma unroll
+        for (int u = 0; u < UB; ++u) {
+          const int64_t vi = v + (int64_t)u * THREADS;
+          if (vi < v1) x[u] = ld_b<BNC>(vin + vi, pol_drop);
+        }
+#pragma unroll
+        for (int u = 0; u < UB; ++u) {
+          const int64_t vi = v + (int64_t)u * THREADS;
+          if (vi < v1) {
+            Acc y[N];
+            if constexpr (kF64) {
+              y[0] = x[u].x * cf;
+              y[1] = x[u].y * cf;
+            } else {  // f32 in: scale in the output's working precision
+              y[0] = static_cast<Acc>(x[u].x) * cf;
+              y[1] = static_cast<Acc>(x[u].y) * cf;
+              y[2] = static_cast<Acc>(x[u].z) * cf;
+              y[3] = static_cast<Acc>(x[u].w) * cf;
+            }
+            put_vec<Tout, N, Acc>(vout + vi * N, y);
+          }
+        }
+      }
+      const int64_t tail0 = sg.head + sg.nv * N;
+      if (c == 0 && t < sg.head) put1(out + t, static_cast<Acc>(in[t]) * cf);
+      if (c == G - 1 && t < sg.n - tail0) put1(out + tail0 + t, static_cast<Acc>(in[tail0 + t]) * cf);
+    } else {
+      const int64_t per = (sg.n + G - 1) / G;
+      const int64_t e0 = min64((int64_t)c * per, sg.n), e1 = min64(e0 + per, sg.n);
+      for (int64_t e = e0 + t; e < e1; e += THREADS) put1(out + e, static_cast<Acc>(in[e]) * cf);
+    }
+  };
+
+  for (int it = 0; it < p.nseg + (scale ? LAG : 0); ++it) {
+    if (it < p.nseg) norm_pass(it);
+    if (scale && it >= LAG) scale_pass(it - LAG);
+  }
+  if (!scale)  // norm-only: publish every segment, spread over CTAs
+    for (int s = c; s < p.nseg; s += G) fold(s, true);
+
+  __syncthreads();
+  if (t == 0) {
+    if (atom_add_acq_rel_u32(&p.counters[kMaxSegs], 1u) == (unsigned)G - 1) {
+      for (int s = 0; s < p.nseg; ++s) p.counters[s] = 0u;
+      p.counters[kMaxSegs] = 0u;
+      __threadfence();
+    }
+  }
+}
+
+template <typename Tin, typename Tout, int THREADS, int CPS, int LAG, int UA, int UB, int BNC>
+int launch_l2lag(ClipParams& p, cudaStream_t stream) {
+  auto kern = k_bucket_clip_l2lag<Tin, Tout, THREADS, CPS, LAG, UA, UB, BNC>;
   const DeviceInfo& di = device_info();
   B2_REQUIRE(di.coop, B2_ERR_CUDA, "device does not support cooperative launch");
-  int occ = 0;
-  B2_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, 0));
-  B2_REQUIRE(occ >= 1, B2_ERR_CUDA, "bucket_clip kernel cannot be resident");
-  int per_sm = ctas_per_sm > 0 ? std::min(ctas_per_sm, occ) : std::min(2, occ);
-  int grid = std::min(per_sm * di.sm_count, kMaxGrid);
-  // small problems: fewer CTAs (each still gets >= kThreads*kUnroll vectors)
+  static int occ_cached[64] = {};
+  int& occ = occ_cached[di.device & 63];
+  if (occ == 0) {
+    B2_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, THREADS, 0));
+    B2_REQUIRE(occ >= 1, B2_ERR_CUDA, "clip kernel cannot be resident");
+  }
   int64_t total = 0;
   for (int s = 0; s < p.nseg; ++s) total += p.seg[s].n;
-  const int64_t want = (total + (int64_t)kThreads * kUnroll * 4 - 1) / ((int64_t)kThreads * kUnroll * 4);
-  grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid, want));
-  void* args[] = {&p};
-  B2_CHECK(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kThreads), args, 0, stream));
+  const int64_t want = (total + 16384 - 1) / 16384;  // small problems: fewer CTAs
+  const int grid = (int)std::max<int64_t>(
+      1, std::min<int64_t>({(int64_t)di.sm_count * std::min(CPS, occ), want, (int64_t)kMaxGrid}));
+  const int N = p.seg_vec_elems;
+  for (int s = 0; s < p.nseg; ++s) {
+    Seg& sg = p.seg[s];
+    sg.nv = sg.vec ? (sg.n - sg.head) / N : 0;
+    sg.per = (sg.nv + grid - 1) / grid;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // CTAs wait on each other's partials
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  B2_CHECK(cudaLaunchKernelEx(&cfg, kern, p));
   return B2_OK;
+}
+
+constexpr int kRingPieces = 13;  // 13 x 16 KB = 208 KB ring (+ barriers) per SM
+constexpr int kPiece = 16384;
+
+template <typename Tin, typename Tout, int LAG, int MODE>
+int launch_clip_tma_lag(ClipParams& p, cudaStream_t stream) {
+  auto kern = k_bucket_clip_tma<Tin, Tout, kRingPieces, kPiece, LAG, MODE>;
+  const DeviceInfo& di = device_info();
+  B2_REQUIRE(di.coop, B2_ERR_CUDA, "device does not support cooperative launch");
+  constexpr int smem = MODE == 2 ? 0 : kRingPieces * (kPiece + 16);
+  static bool configured[64] = {};
+  if (!configured[di.device & 63]) {  // one-time per device and instantiation
+    B2_CHECK(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int occ = 0;
+    B2_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kTThreads + 32, smem));
+    B2_REQUIRE(occ >= 1, B2_ERR_CUDA, "TMA clip kernel cannot be resident");
+    configured[di.device & 63] = true;
+  }
+  int64_t total = 0;
+  for (int s = 0; s < p.nseg; ++s) total += p.seg[s].n;
+  // small problems use fewer CTAs (>= four 16 KB pieces of elements each)
+  const int64_t want = (total + 16384 - 1) / 16384;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)di.sm_count, want, (int64_t)kMaxGrid}));
+  const int N = p.seg_vec_elems;
+  for (int s = 0; s < p.nseg; ++s) {  // per-CTA chunk geometry (host-side division)
+    Seg& sg = p.seg[s];
+    sg.nv = sg.vec ? (sg.n - sg.head) / N : 0;
+    sg.per = (sg.nv + grid - 1) / grid;
+  }
+  // cooperative (all CTAs co-resident: they wait on each other's partials);
+  // cudaLaunchKernelEx keeps the launch capturable into CUDA graphs
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kTThreads + 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  B2_CHECK(cudaLaunchKernelEx(&cfg, kern, p));
+  return B2_OK;
+}
+
+static int clip_cfg() {
+  // tuning knob: B2_CLIP_CFG selects a K1 configuration (see launch_clip_tma)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("B2_CLIP_CFG");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
+// K1 configuration: THREADS x CTAs/SM, lag, stream-A / stream-B loads in
+// flight per thread (tools/clip_bench.py sweeps; measurements in DESIGN.md).
+// B2_CLIP_CFG=5 selects the TMA-ring variant for A/B comparisons.
+template <typename Tin, typename Tout>
+int launch_clip_k1(ClipParams& p, cudaStream_t stream) {
+  if constexpr (std::is_same<Tin, float>::value && std::is_same<Tout, __nv_bfloat16>::value) {
+    switch (clip_cfg()) {
+      case 5: return launch_clip_tma_lag<Tin, Tout, 1, 0>(p, stream);
+      case 8: return launch_l2lag<Tin, Tout, 256, 3, 1, 8, 4, 0>(p, stream);
+      case 9: return launch_l2lag<Tin, Tout, 512, 2, 1, 4, 4, 0>(p, stream);
+      case 11: return launch_l2lag<Tin, Tout, 384, 2, 1, 8, 2, 0>(p, stream);
+      default: break;
+    }
+  }
+  return launch_l2lag<Tin, Tout, 384, 2, 1, 8, 4, 0>(p, stream);
 }
 
 // ---------------------------------------------------------------- K1b
@@ -403,6 +869,7 @@ extern "C" int b2_bucket_clip_cast(const void* in, int in_dtype, void* out, int 
     p.coef_ws = reinterpret_cast<double*>(wsb + WsLayout::coef);
     p.counters = reinterpret_cast<unsigned*>(wsb + WsLayout::counters);
     p.nseg = std::min(kMaxSegs, nseg - s0);
+    p.seg_vec_elems = N;
     for (int i = 0; i < p.nseg; ++i) {
       Seg& sg = p.seg[i];
       const int s = s0 + i;
@@ -428,10 +895,10 @@ extern "C" int b2_bucket_clip_cast(const void* in, int in_dtype, void* out, int 
     }
     int rc = B2_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    if (in_dtype == B2_F64) rc = launch_clip<double, double>(p, ctas_per_sm, st);
-    else if (out == nullptr || out_dtype == B2_F32) rc = launch_clip<float, float>(p, ctas_per_sm, st);
-    else if (out_dtype == B2_BF16) rc = launch_clip<float, __nv_bfloat16>(p, ctas_per_sm, st);
-    else rc = launch_clip<float, double>(p, ctas_per_sm, st);
+    if (in_dtype == B2_F64) rc = launch_clip_k1<double, double>(p, st);
+    else if (out == nullptr || out_dtype == B2_F32) rc = launch_clip_k1<float, float>(p, st);
+    else if (out_dtype == B2_BF16) rc = launch_clip_k1<float, __nv_bfloat16>(p, st);
+    else rc = launch_clip_k1<float, double>(p, st);
     if (rc != B2_OK) return rc;
   }
   return B2_OK;

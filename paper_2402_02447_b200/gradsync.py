@@ -171,6 +171,12 @@ class BucketClipper:
     def clip_cast(self, grad: torch.Tensor, out: torch.Tensor | None, segments: Sequence,
                   limit: float, post_scale: float = 1.0, norms: torch.Tensor | None = None,
                   coefs: torch.Tensor | None = None, nonfinite: torch.Tensor | None = None) -> None:
+        self.prepare(grad, out, segments, limit, post_scale, norms, coefs, nonfinite)()
+
+    def prepare(self, grad: torch.Tensor, out: torch.Tensor | None, segments: Sequence,
+                limit: float, post_scale: float = 1.0, norms: torch.Tensor | None = None,
+                coefs: torch.Tensor | None = None, nonfinite: torch.Tensor | None = None):
+        """Validate once and return a zero-argument launcher (per-bucket hot loops, graph capture)."""
         segs = list(segments)
         if grad.dtype not in (torch.float32, torch.float64) or not grad.is_cuda:
             raise ValueError("grad must be a CUDA float32/float64 tensor")
@@ -189,7 +195,8 @@ class BucketClipper:
         outs = _lib.i64_array(s[1] for s in segs)
         lens = _lib.i64_array(s[2] for s in segs)
         ws = self.workspace
-        rc = self.lib.b2_bucket_clip_cast(
+        fn = self.lib.b2_bucket_clip_cast
+        args = (
             grad.data_ptr(), _DT[grad.dtype],
             out.data_ptr() if out is not None else None, _DT[out.dtype] if out is not None else 0,
             ins, outs, lens, len(segs), float(limit), float(post_scale),
@@ -198,7 +205,14 @@ class BucketClipper:
             nonfinite.data_ptr() if nonfinite is not None else None,
             ws.data_ptr(), ws.numel(), self.ctas_per_sm, self._sp(),
         )
-        _lib.check(rc)
+        keep = (grad, out, norms, coefs, nonfinite, ws)  # tensors must outlive the launcher
+        check = _lib.check
+
+        def launch():
+            check(fn(*args))
+            return keep
+
+        return launch
 
     def weighted_mean(self, mat: torch.Tensor, coefs: torch.Tensor, bounds: Sequence[int],
                       out: torch.Tensor) -> None:
@@ -225,7 +239,12 @@ def _clipper() -> BucketClipper:
 
 
 def _result(t: torch.Tensor, host: bool):
-    return t.cpu().numpy() if host else t
+    """Host callers get numpy; the D2H lands in (cached) pinned memory at full PCIe rate."""
+    if not host:
+        return t
+    dst = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    dst.copy_(t)
+    return dst.numpy()
 
 
 def _raise_if_flagged(flags: torch.Tensor) -> None:

@@ -33,6 +33,7 @@ BUCKET = ClipConfig(1.0, "bucket_wise")
 BEFORE = ClipConfig(1.0, "before_allreduce")
 AFTER = ClipConfig(1.0, "after_allreduce")
 F32_REL = 1e-5
+F64_REL = 1e-12
 
 
 def rel_err(a, b):
@@ -55,10 +56,11 @@ def test_golden_fp64_path(h1_golden):
         layout = [tuple(x) for x in g[f"c{i}_layout"]]
         out = sync_bucketwise(GradientState(w, layout), BUCKET)
         assert isinstance(out, np.ndarray) and out.dtype == np.float64
-        np.testing.assert_allclose(out, g[f"c{i}_out"], rtol=1e-12, atol=1e-300)
+        # fp64 device path: 1e-12 of the vector's scale (norms differ from OpenBLAS ddot in the last bits)
+        assert rel_err(out, g[f"c{i}_out"]) <= F64_REL, i
         if f"c{i}_before" in g:
-            np.testing.assert_allclose(sync_before(GradientState(w, layout), BEFORE), g[f"c{i}_before"], rtol=1e-12)
-            np.testing.assert_allclose(sync_after(GradientState(w, layout), AFTER), g[f"c{i}_after"], rtol=1e-12)
+            assert rel_err(sync_before(GradientState(w, layout), BEFORE), g[f"c{i}_before"]) <= F64_REL
+            assert rel_err(sync_after(GradientState(w, layout), AFTER), g[f"c{i}_after"]) <= F64_REL
 
 
 def test_golden_fp32_device_path(h1_golden):
@@ -79,7 +81,9 @@ def test_golden_norms(h1_golden):
         w = g[f"c{i}_workers"]
         layout = [tuple(x) for x in g[f"c{i}_layout"]]
         K = w.shape[0]
-        for dt, tol in ((torch.float64, 1e-13), (torch.float32, 1e-12)):
+        # fp64 input: exact fp64 accumulation; fp32 input: fp32 mini-sums of <= 8
+        # squares promoted to fp64 (rel. error well below the 1e-5 contract)
+        for dt, tol in ((torch.float64, 1e-13), (torch.float32, 1e-6)):
             wt = torch.tensor(w, dtype=dt, device="cuda")
             segs = [(k * w.shape[1] + a, 0, b - a) for k in range(K) for a, b in layout]
             norms = torch.empty(len(segs), dtype=torch.float64, device="cuda")
@@ -144,10 +148,10 @@ def test_cross_mode_properties():
         w = rng.normal(size=(k, d)) * float(rng.choice([0.01, 1.0, 100.0]))
         out = sync_bucketwise(state(w, b), BUCKET)
         assert np.linalg.norm(out) <= 1.0 + 1e-9
-        np.testing.assert_allclose(out, O.sync_bucketwise(w, equal_bucket_layout(d, b), 1.0), rtol=1e-12, atol=1e-300)
+        assert rel_err(out, O.sync_bucketwise(w, equal_bucket_layout(d, b), 1.0)) <= F64_REL
     # B = 1 equals before-allreduce (acceptance criterion 2)
     w = rng.normal(size=(4, 10)) * 3
-    np.testing.assert_allclose(sync_bucketwise(state(w, 1), BUCKET), sync_before(state(w), BEFORE), rtol=1e-12)
+    assert rel_err(sync_bucketwise(state(w, 1), BUCKET), sync_before(state(w), BEFORE)) <= F64_REL
     # below-threshold transparency is exact (test_gradsync.py:176-182)
     w = rng.normal(size=(5, 12))
     w *= 0.4 / (2 * np.sqrt(12) * np.abs(w).max())
@@ -181,11 +185,33 @@ def test_alignment_and_odd_sizes():
             c.clip_cast(g, out, [(a, a, b - a) for a, b in layout], 0.3, norms=norms, coefs=coefs)
             gh = g.double().cpu().numpy()
             rn, rc = O.bucket_coefficients(gh, layout, 0.3)
-            np.testing.assert_allclose(norms.cpu().numpy(), rn, rtol=1e-12)
-            np.testing.assert_allclose(coefs.cpu().numpy(), rc, rtol=1e-12)
+            np.testing.assert_allclose(norms.cpu().numpy(), rn, rtol=1e-6)
+            np.testing.assert_allclose(coefs.cpu().numpy(), rc, rtol=1e-6)
             ref = np.concatenate([gh[a:b] * cf for (a, b), cf in zip(layout, rc)])
             tol = F32_REL if odt == torch.float32 else 2.0 ** -8
             assert rel_err(out.float().cpu().numpy(), ref) <= tol
+
+
+def test_fp32_range_extremes():
+    """Squares that under/overflow fp32 fall back to exact fp64 accumulation."""
+    c = BucketClipper()
+    rng = np.random.default_rng(5)
+    for scale in (1e-30, 1e-22, 1e-3, 1e21, 1e30):
+        x = (rng.normal(size=300_000) * scale).astype(np.float32)
+        g = torch.from_numpy(x).cuda()
+        layout = [(0, 1000), (1000, 200_000), (200_000, 300_000)]
+        norms = torch.empty(3, dtype=torch.float64, device="cuda")
+        flags = torch.empty(3, dtype=torch.int32, device="cuda")
+        out = torch.empty_like(g)
+        c.clip_cast(g, out, [(a, a, b - a) for a, b in layout], 1.0, norms=norms, nonfinite=flags)
+        rn = O.bucket_norms(x.astype(np.float64), layout)
+        np.testing.assert_allclose(norms.cpu().numpy(), rn, rtol=1e-6)
+        assert flags.cpu().tolist() == [0, 0, 0]
+    x = np.ones(100_000, dtype=np.float32)
+    x[77_777] = np.inf
+    flags = torch.empty(2, dtype=torch.int32, device="cuda")
+    c.clip_cast(torch.from_numpy(x).cuda(), None, [(0, 0, 50_000), (50_000, 0, 50_000)], 1.0, nonfinite=flags)
+    assert flags.cpu().tolist() == [0, 1]
 
 
 def test_workspace_reuse_and_determinism():
@@ -210,7 +236,7 @@ def test_many_segments_multi_launch():
     w = rng.normal(size=(3, 300 * 5)) * 0.05
     layout = equal_bucket_layout(w.shape[1], 300)
     out = sync_bucketwise(GradientState(w, layout), BUCKET)
-    np.testing.assert_allclose(out, O.sync_bucketwise(w, layout, 1.0), rtol=1e-12, atol=1e-300)
+    assert rel_err(out, O.sync_bucketwise(w, layout, 1.0)) <= F64_REL
 
 
 # ------------------------------------------------------------- full BASELINE sizes
@@ -229,9 +255,9 @@ def test_bert_sized_parity(dim):
     c.clip_cast(g, out16, segs, limit)
     gh = g.cpu().numpy()
     rnorm = np.array([np.linalg.norm(gh[a:b].astype(np.float64)) for a, b in reversed(layout)])
-    np.testing.assert_allclose(norms.cpu().numpy(), rnorm, rtol=1e-10)
+    np.testing.assert_allclose(norms.cpu().numpy(), rnorm, rtol=1e-6)
     rcoef = np.where(rnorm >= limit, limit / rnorm, 1.0)
-    np.testing.assert_allclose(coefs.cpu().numpy(), rcoef, rtol=1e-10)
+    np.testing.assert_allclose(coefs.cpu().numpy(), rcoef, rtol=1e-6)
     clipped = rcoef < 1.0
     assert 0 < clipped.sum() < B  # the seeded scale mix clips some buckets, not all
     o32 = out32.cpu().numpy()
