@@ -4,9 +4,10 @@
 
 N>1 is launched by the driver under torchrun (one rank per GPU, NCCL).  Rank 0
 prints ONE JSON line.  Headline (`value`): whole-job fp32 gradient GB/s
-through the bucket-wise clip (K1, one launch per 25 MiB bucket in backward
-order) + per-bucket NCCL average of the bf16 comm buffer on a side stream
-(N>1), inputs resident in HBM (1.34 GB per rank > 126 MB L2, so no flush is
+through the bucket-wise clip — at N=1 one fused K1 launch over the 52
+buckets (nothing to reduce), at N>1 one K1 launch per 25 MiB bucket in
+backward order + an NCCL average of that bf16 bucket on a side stream —
+inputs resident in HBM (1.34 GB per rank > 126 MB L2, so no flush is
 needed).  `e2e`: the same metric through the public API
 (`GradientState`+`sync_bucketwise`, or `BucketwiseSync` at N>1) from pinned
 host gradients to a host result.  `presort`: stratified local presort of 10M
@@ -136,6 +137,15 @@ def barrier(world: int):
 
 
 # --------------------------------------------------------------------- H1 (ours)
+def ncu_traffic(kernel_key: str):
+    """dram read+write bytes per launch of `kernel_key` from the committed ncu summary, if any."""
+    f = ROOT / "profiles" / "ncu_summary.json"
+    if not f.exists():
+        return None
+    d = json.loads(f.read_text()).get(kernel_key)
+    return None if d is None else d.get("dram_bytes_per_launch")
+
+
 def bench_clip(args, rank, world, local):
     import torch
     import torch.distributed as dist
@@ -148,26 +158,38 @@ def bench_clip(args, rank, world, local):
     g, layout, scales = synthetic.bert_grads(dim, rank=rank)
     nb = len(layout)
     cfg = B.ClipConfig(1.0, "bucket_wise")
-    limit = 1.0 / math.sqrt(nb)
-    clip = B.BucketClipper()
+    limit = 1.0 / math.sqrt(nb)  # c / sqrt(B), gradsync.py:155
     comm = torch.empty(dim, dtype=torch.bfloat16, device="cuda")
     compute = torch.cuda.current_stream()
     side = torch.cuda.Stream()
     evs = [torch.cuda.Event() for _ in range(nb)]
-    op = dist.ReduceOp.AVG if world > 1 else None
-    order = list(reversed(range(nb)))
+    order = list(reversed(range(nb)))  # backward order, gradsync.py:157
+    segs = [(layout[b][0], layout[b][0], layout[b][1] - layout[b][0]) for b in order]
+    clip = B.BucketClipper()
 
-    def step():
-        for b in order:
-            a, e = layout[b]
-            clip.clip_cast(g, comm, [(a, a, e - a)], limit)
-            if world > 1:
+    if world == 1:
+        # all buckets resident: one fused launch over the 52 buckets (sync_bucketwise path)
+        launch_all = clip.prepare(g, comm, segs, limit)
+
+        def step():
+            launch_all()
+        mode = "one fused K1 launch over all 52 buckets (no allreduce at N=1)"
+        launches_per_step = 1
+    else:
+        # per-bucket K1 on the compute stream, NCCL average of the bf16 bucket on a side stream
+        per_bucket = [clip.prepare(g, comm, [s], limit) for s in segs]
+
+        def step():
+            for i, b in enumerate(order):
+                a, e = layout[b]
+                per_bucket[i]()
                 evs[b].record(compute)
                 side.wait_event(evs[b])
                 with torch.cuda.stream(side):
-                    dist.all_reduce(comm[a:e], op=op)
-        if world > 1:
+                    dist.all_reduce(comm[a:e], op=dist.ReduceOp.AVG)
             compute.wait_stream(side)
+        mode = "per-bucket K1 + ncclAllReduce(avg, bf16) per bucket on a side stream"
+        launches_per_step = nb
 
     for _ in range(args.warmup):
         step()
@@ -175,7 +197,11 @@ def bench_clip(args, rank, world, local):
     barrier(world)
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
+        # keep the GPU loaded ~0.6 s so the sampler sees clocks under load, then time
+        tl = time.perf_counter()
+        while time.perf_counter() - tl < 0.6:
+            step()
+            torch.cuda.synchronize()
         barrier(world)
         t0.record(compute)
         for _ in range(args.steps):
@@ -185,47 +211,62 @@ def bench_clip(args, rank, world, local):
         barrier(world)
     ms = max_over_ranks(t0.elapsed_time(t1) / args.steps, world)
 
-    # K1 alone (the dominant kernel at N=1): CUDA events around the same launches
+    # dominant kernel alone: the fused launch over all buckets, CUDA events on its stream
+    launch_all = clip.prepare(g, comm, segs, limit)
     k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    k0.record(compute)
-    for _ in range(args.steps):
-        for b in order:
-            a, e = layout[b]
-            clip.clip_cast(g, comm, [(a, a, e - a)], limit)
-    k1.record(compute)
-    torch.cuda.synchronize()
-    k_ms_step = k0.elapsed_time(k1) / args.steps
-    k_ms_launch = k_ms_step / nb
-    # batched variant: all 52 buckets in one cooperative launch (sync_bucketwise path)
-    segs = [(layout[b][0], layout[b][0], layout[b][1] - layout[b][0]) for b in order]
     for _ in range(3):
-        clip.clip_cast(g, comm, segs, limit)
+        launch_all()
     torch.cuda.synchronize()
     k0.record(compute)
     for _ in range(args.steps):
-        clip.clip_cast(g, comm, segs, limit)
+        launch_all()
     k1.record(compute)
     torch.cuda.synchronize()
     kb_ms = k0.elapsed_time(k1) / args.steps
+    # per-bucket launches (DDP-hook shape), captured once in a CUDA graph
+    pb = {}
+    try:
+        gside = torch.cuda.Stream()
+        gside.wait_stream(compute)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(gside):
+            gclip = B.BucketClipper(stream=gside)
+            torch.cuda.synchronize()
+            with torch.cuda.graph(graph, stream=gside):
+                for s_ in segs:
+                    gclip.prepare(g, comm, [s_], limit)()
+        torch.cuda.synchronize()
+        for _ in range(3):
+            graph.replay()
+        torch.cuda.synchronize()
+        k0.record(compute)
+        for _ in range(args.steps):
+            graph.replay()
+        k1.record(compute)
+        torch.cuda.synchronize()
+        pb_ms = k0.elapsed_time(k1) / args.steps
+        pb = {"us_per_step": pb_ms * 1e3, "us_per_launch": pb_ms * 1e3 / nb,
+              "achieved_gbs": dim * 6 / (pb_ms * 1e-3) / 1e9, "launches": nb, "cuda_graph": True}
+    except Exception as e:  # graph capture unavailable: report, do not fail the bench
+        pb = {"error": str(e)[:200]}
 
     pk = peaks()
-    alg_bytes_step = dim * (4 + 2)  # fp32 read + bf16 write
-    k_gbs = alg_bytes_step / (k_ms_step * 1e-3) / 1e9
-    kb_gbs = alg_bytes_step / (kb_ms * 1e-3) / 1e9
+    alg_bytes = dim * (4 + 2)  # fp32 read + bf16 write per element
+    kb_gbs = alg_bytes / (kb_ms * 1e-3) / 1e9
+    traffic = ncu_traffic("k_bucket_clip_l2lag<float,bf16>/bert_large_52")
     res = {
         "ms_per_step": ms,
         "value": world * dim * 4 / (ms * 1e-3) / 1e9,
+        "mode": mode,
         "roofline": {
-            "bound": "hbm", "kernel": "k_bucket_clip<f32,bf16> (one launch per 25 MiB bucket)",
-            "achieved": k_gbs, "peak": pk["hbm_gbs"], "peak_src": pk["src"], "unit": "GB/s",
-            "frac": k_gbs / pk["hbm_gbs"], "traffic": None,
-            "bytes_per_launch": alg_bytes_step / nb, "launch_us": k_ms_launch * 1e3,
-            "batched_one_launch": {"achieved": kb_gbs, "frac": kb_gbs / pk["hbm_gbs"], "us": kb_ms * 1e3},
+            "bound": "hbm", "kernel": "k_bucket_clip_l2lag<f32,bf16>: one launch, 52 x 25 MiB buckets",
+            "achieved": kb_gbs, "peak": pk["hbm_gbs"], "peak_src": pk["src"], "unit": "GB/s",
+            "frac": kb_gbs / pk["hbm_gbs"], "traffic": traffic, "bytes_per_launch": alg_bytes,
+            "launch_us": kb_ms * 1e3,
+            "per_bucket_launches": pb,
         },
-        "gpu_launches": args.steps * nb,
+        "gpu_launches": args.steps * launches_per_step,
         "clocks": clk.summary(),
-        "clipped_buckets": int(sum(1 for a, b in layout if False)),
     }
     if world > 1:
         algbw = dim * 2 / (ms * 1e-3) / 1e9
@@ -233,7 +274,7 @@ def bench_clip(args, rank, world, local):
                          "peak_gbs": 900.0, "busbw_frac": algbw * 2 * (world - 1) / world / 900.0,
                          "comm_dtype": "bf16", "collective": "ncclAllReduce avg per bucket, side stream"}
 
-    # e2e: pinned host fp32 gradients -> device -> sync -> host result
+    # e2e: pinned host fp32 gradients -> device -> sync -> host result, through the public API
     host = torch.empty((1, dim), dtype=torch.float32, pin_memory=True)
     host.copy_(g.view(1, -1).cpu())
     e2e_steps = max(2, min(args.steps, 5))
@@ -242,6 +283,7 @@ def bench_clip(args, rank, world, local):
             st = B.GradientState(host, layout)
             return B.sync_bucketwise(st, cfg)
         d2h = dim * 4
+        api = "GradientState + sync_bucketwise (pinned host fp32 in, host fp32 out)"
     else:
         sync = BucketwiseSync(layout, cfg, comm_dtype=torch.bfloat16)
         out_host = torch.empty(dim, dtype=torch.bfloat16, pin_memory=True)
@@ -253,6 +295,7 @@ def bench_clip(args, rank, world, local):
             torch.cuda.current_stream().synchronize()
             return out_host
         d2h = dim * 2
+        api = "BucketwiseSync.sync (pinned host fp32 in, host bf16 out)"
     e2e_step()
     torch.cuda.synchronize()
     barrier(world)
@@ -260,14 +303,10 @@ def bench_clip(args, rank, world, local):
     for _ in range(e2e_steps):
         e2e_step()
     torch.cuda.synchronize()
-    e2e_s = max_over_ranks((time.perf_counter() - ts) / e2e_steps, world)
+    e2e_s = max_over_ranks(time.perf_counter() - ts, world) / e2e_steps
     res["e2e"] = {"value": world * dim * 4 / e2e_s / 1e9, "unit": "GB/s", "ms_per_step": e2e_s * 1e3,
-                  "h2d_bytes_per_step": dim * 4, "d2h_bytes_per_step": d2h, "steps": e2e_steps,
-                  "api": "GradientState+sync_bucketwise (host fp32 in, host fp32 out)" if world == 1
-                  else "BucketwiseSync.sync (host fp32 in, host bf16 out)"}
-    gh = g[: layout[0][1]].cpu().numpy()
-    res["_cpu_sample"] = gh  # first bucket for the CPU baseline
-    res["_scales"] = scales
+                  "h2d_bytes_per_step": dim * 4, "d2h_bytes_per_step": d2h, "steps": e2e_steps, "api": api}
+    res["_cpu_sample"] = g[: layout[0][1]].cpu().numpy()  # first bucket for the CPU baseline
     del host
     return res
 
@@ -463,8 +502,6 @@ def main():
     rank, world, local = dist_init(args.gpus)
     r = bench_clip(args, rank, world, local)
     sample = r.pop("_cpu_sample")
-    r.pop("_scales")
-    r.pop("clipped_buckets")
     presort = None
     if rank == 0 and not args.no_presort:
         presort = bench_presort(args)
@@ -476,6 +513,7 @@ def main():
             "data": "synthetic",
             "config": {"workload": "BERT-large synthetic gradients (D=335,141,888 fp32, 52 x 25 MiB buckets), "
                                    "bucket-wise clip c/sqrt(52) + bf16 NCCL avg allreduce per bucket",
+                       "step": r["mode"],
                        "global_batch": None, "parallelism": f"dp{world}",
                        "l2": "inputs 1.34 GB/rank > 126 MB L2 (no flush needed)"},
             "roofline": r["roofline"], "e2e": r["e2e"], "gpu_launches": r["gpu_launches"], "clocks": r["clocks"],

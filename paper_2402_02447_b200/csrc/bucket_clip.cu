@@ -709,6 +709,267 @@ int launch_l2lag(ClipParams& p, cudaStream_t stream) {
   return B2_OK;
 }
 
+// ----------------------------------------------------------------------------
+// K1 (warp-specialised L2-lag): the same two streams as k_bucket_clip_l2lag,
+// but run CONCURRENTLY by two warp groups of every CTA: AT threads stream the
+// norm pass of bucket s while BT threads scale bucket s-1 out of L2.  The
+// groups sync only through named barriers of their own and one shared
+// counter (A may run at most LAG+1 buckets ahead of B, which bounds the L2
+// footprint to ~2 buckets), so HBM reads (A), L2 re-reads and HBM writes (B)
+// overlap instead of alternating.
+template <int NTH>
+__device__ __forceinline__ void group_sync(int id) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(NTH) : "memory");
+}
+
+template <int NTH>
+__device__ __forceinline__ double group_sum(double v, double* scratch, int gt, int bar) {
+  constexpr int W = NTH / 32;
+  const int lane = gt & 31, w = gt >> 5;
+  v = warp_sum(v);
+  group_sync<NTH>(bar);
+  if (lane == 0) scratch[w] = v;
+  group_sync<NTH>(bar);
+  double r = 0.0;
+  if (w == 0) {
+    r = lane < W ? scratch[lane] : 0.0;
+    r = warp_sum(r);
+  }
+  return r;  // valid in the group's warp 0
+}
+
+template <typename Tin, typename Tout, int AT, int BT, int CPS, int LAG, int UA, int UB>
+__global__ void __launch_bounds__(AT + BT, CPS) k_bucket_clip_ws(const __grid_constant__ ClipParams p) {
+  using V = typename VecOf<Tin>::V;
+  constexpr int N = VecOf<Tin>::N;
+  constexpr bool kF64 = std::is_same<Tin, double>::value;
+  using Acc = typename std::conditional<std::is_same<Tin, double>::value || std::is_same<Tout, double>::value,
+                                        double, float>::type;
+  constexpr int kBarA = 1, kBarB = 2;
+  __shared__ double redA[32], redB[32];
+  __shared__ double s_coef;
+  __shared__ volatile int s_bdone;  // buckets the B group has finished
+  const int G = gridDim.x, c = blockIdx.x, t = threadIdx.x;
+  const bool scale = p.out != nullptr;
+  if (t == 0) s_bdone = 0;
+  __syncthreads();
+
+  // fixed-order fold of segment s's G partials by a group of NTH threads
+  auto fold = [&](auto nth, int gt, int bar, double* scratch, int s, bool publish) -> double {
+    constexpr int NTH = decltype(nth)::value;
+    if (gt == 0) {
+      unsigned ns = 32;
+      while (ld_acquire_u32(&p.counters[s]) < (unsigned)G) {
+        __nanosleep(ns);
+        if (ns < 256) ns <<= 1;
+      }
+    }
+    group_sync<NTH>(bar);
+    double v = 0.0;
+    for (int j = gt; j < G; j += NTH) v += __ldcg(&p.partials[(size_t)s * G + j]);
+    const double total = group_sum<NTH>(v, scratch, gt, bar);
+    double coef = 1.0;
+    if (gt == 0) {
+      const double norm = sqrt(total);
+      coef = (norm >= p.limit) ? p.limit / norm : 1.0;  // gradsync.py:114-116
+      if (publish) {
+        if (p.norms) p.norms[s] = norm;
+        if (p.coefs) p.coefs[s] = coef;
+        if (p.nonfinite) p.nonfinite[s] = (kF64 ? isnan(total) : !isfinite(total)) ? 1 : 0;
+      }
+    }
+    return coef;  // valid in gt == 0
+  };
+
+  if (t < AT) {
+    // ================= A group: norm pass, bucket after bucket
+    const int gt = t;
+    const uint64_t pol_keep = scale ? l2_policy_evict_last() : l2_policy_evict_first();
+    for (int s = 0; s < p.nseg; ++s) {
+      if (scale && s > LAG) {  // L2 footprint bound: wait until B finished bucket s-LAG-1
+        if (gt == 0) {
+          unsigned ns = 32;
+          while (s_bdone < s - LAG) {
+            __nanosleep(ns);
+            if (ns < 256) ns <<= 1;
+          }
+        }
+        group_sync<AT>(kBarA);
+      }
+      const Seg sg = p.seg[s];
+      const Tin* in = static_cast<const Tin*>(p.in) + sg.in_off;
+      double acc[N];
+#pragma unroll
+      for (int u = 0; u < N; ++u) acc[u] = 0.0;
+      bool bad = false;
+      auto add = [&](const V& x) {
+        double e[N];
+        unpack(x, e);
+#pragma unroll
+        for (int u = 0; u < N; ++u) {
+          if constexpr (kF64) bad |= !isfinite(e[u]);
+          acc[u] = fma(e[u], e[u], acc[u]);
+        }
+      };
+      if (sg.vec) {
+        const V* vin = reinterpret_cast<const V*>(in + sg.head);
+        const int64_t v0 = min64((int64_t)c * sg.per, sg.nv), v1 = min64(v0 + sg.per, sg.nv);
+        for (int64_t v = v0 + gt; v < v1; v += (int64_t)AT * UA) {
+          V x[UA];
+#pragma unroll
+          for (int u = 0; u < UA; ++u) {
+            const int64_t vi = v + (int64_t)u * AT;
+            x[u] = vi < v1 ? ld_a<0>(vin + vi, pol_keep) : V{};
+          }
+          if constexpr (kF64) {
+#pragma unroll
+            for (int u = 0; u < UA; ++u) add(x[u]);
+          } else {
+            // f32: <= 32 squares summed in fp32 (rel. error < 2e-6), promoted
+            // once; a mini-sum outside [2^-100, 2^100] with a non-zero element
+            // (underflow, overflow, inf, nan) is redone exactly in fp64
+#pragma unroll
+            for (int h = 0; h < UA; h += 8) {
+              float m = 0.0f;
+              unsigned nz = 0;
+#pragma unroll
+              for (int u = h; u < h + 8 && u < UA; ++u) {
+                m = fmaf(x[u].x, x[u].x, m);
+                m = fmaf(x[u].y, x[u].y, m);
+                m = fmaf(x[u].z, x[u].z, m);
+                m = fmaf(x[u].w, x[u].w, m);
+                nz |= __float_as_uint(x[u].x) | __float_as_uint(x[u].y) | __float_as_uint(x[u].z) |
+                      __float_as_uint(x[u].w);
+              }
+              if (m >= 0x1p-100f && m <= 0x1p100f) {
+                acc[0] += (double)m;
+              } else if ((nz << 1) != 0u) {
+#pragma unroll
+                for (int u = h; u < h + 8 && u < UA; ++u) add(x[u]);
+              }
+            }
+          }
+        }
+        const int64_t tail0 = sg.head + sg.nv * N;
+        if (c == 0 && gt < sg.head) acc[0] += sq_of(in[gt], bad);
+        if (c == G - 1 && gt < sg.n - tail0) acc[N - 1] += sq_of(in[tail0 + gt], bad);
+      } else {
+        const int64_t per = (sg.n + G - 1) / G;
+        const int64_t e0 = min64((int64_t)c * per, sg.n), e1 = min64(e0 + per, sg.n);
+        for (int64_t e = e0 + gt; e < e1; e += AT) acc[0] += sq_of(in[e], bad);
+      }
+      double part = 0.0;
+#pragma unroll
+      for (int u = 0; u < N; ++u) part += acc[u];
+      if constexpr (kF64) part = __any_sync(0xffffffffu, bad) ? __longlong_as_double(0x7ff8000000000000ll) : part;
+      const double tot = group_sum<AT>(part, redA, gt, kBarA);  // NaN propagates: marks inf/nan input
+      if (gt == 0) {
+        p.partials[(size_t)s * G + c] = tot;
+        red_release_u32(&p.counters[s], 1u);  // fire-and-forget arrival
+      }
+    }
+    if (!scale)  // norm-only: publish every segment, spread over CTAs
+      for (int s = c; s < p.nseg; s += G) fold(std::integral_constant<int, AT>{}, gt, kBarA, redA, s, true);
+  } else if (scale) {
+    // ================= B group: scale pass, one bucket behind
+    const int gt = t - AT;
+    const uint64_t pol_drop = l2_policy_evict_first();
+    for (int s = 0; s < p.nseg; ++s) {
+      const double coef = fold(std::integral_constant<int, BT>{}, gt, kBarB, redB, s, c == 0);
+      if (gt == 0) s_coef = coef;
+      group_sync<BT>(kBarB);
+      const Acc cf = static_cast<Acc>(s_coef * p.post_scale);
+      const Seg sg = p.seg[s];
+      const Tin* in = static_cast<const Tin*>(p.in) + sg.in_off;
+      Tout* out = static_cast<Tout*>(p.out) + sg.out_off;
+      if (sg.vec) {
+        const V* vin = reinterpret_cast<const V*>(in + sg.head);
+        Tout* vout = out + sg.head;
+        const int64_t v0 = min64((int64_t)c * sg.per, sg.nv), v1 = min64(v0 + sg.per, sg.nv);
+        for (int64_t v = v0 + gt; v < v1; v += (int64_t)BT * UB) {
+          V x[UB];
+#pragma unroll
+          for (int u = 0; u < UB; ++u) {
+            const int64_t vi = v + (int64_t)u * BT;
+            if (vi < v1) x[u] = ld_b<0>(vin + vi, pol_drop);
+          }
+#pragma unroll
+          for (int u = 0; u < UB; ++u) {
+            const int64_t vi = v + (int64_t)u * BT;
+            if (vi < v1) {
+              Acc y[N];
+              if constexpr (kF64) {
+                y[0] = x[u].x * cf;
+                y[1] = x[u].y * cf;
+              } else {
+                y[0] = static_cast<Acc>(x[u].x) * cf;
+                y[1] = static_cast<Acc>(x[u].y) * cf;
+                y[2] = static_cast<Acc>(x[u].z) * cf;
+                y[3] = static_cast<Acc>(x[u].w) * cf;
+              }
+              put_vec<Tout, N, Acc>(vout + vi * N, y);
+            }
+          }
+        }
+        const int64_t tail0 = sg.head + sg.nv * N;
+        if (c == 0 && gt < sg.head) put1(out + gt, static_cast<Acc>(in[gt]) * cf);
+        if (c == G - 1 && gt < sg.n - tail0) put1(out + tail0 + gt, static_cast<Acc>(in[tail0 + gt]) * cf);
+      } else {
+        const int64_t per = (sg.n + G - 1) / G;
+        const int64_t e0 = min64((int64_t)c * per, sg.n), e1 = min64(e0 + per, sg.n);
+        for (int64_t e = e0 + gt; e < e1; e += BT) put1(out + e, static_cast<Acc>(in[e]) * cf);
+      }
+      group_sync<BT>(kBarB);  // whole group done with bucket s (also retires s_coef)
+      if (gt == 0) s_bdone = s + 1;
+    }
+  }
+
+  __syncthreads();
+  if (t == 0) {
+    if (atom_add_acq_rel_u32(&p.counters[kMaxSegs], 1u) == (unsigned)G - 1) {
+      for (int s = 0; s < p.nseg; ++s) p.counters[s] = 0u;
+      p.counters[kMaxSegs] = 0u;
+      __threadfence();
+    }
+  }
+}
+
+template <typename Tin, typename Tout, int AT, int BT, int CPS, int LAG, int UA, int UB>
+int launch_ws(ClipParams& p, cudaStream_t stream) {
+  auto kern = k_bucket_clip_ws<Tin, Tout, AT, BT, CPS, LAG, UA, UB>;
+  const DeviceInfo& di = device_info();
+  B2_REQUIRE(di.coop, B2_ERR_CUDA, "device does not support cooperative launch");
+  static int occ_cached[64] = {};
+  int& occ = occ_cached[di.device & 63];
+  if (occ == 0) {
+    B2_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, AT + BT, 0));
+    B2_REQUIRE(occ >= 1, B2_ERR_CUDA, "clip kernel cannot be resident");
+  }
+  int64_t total = 0;
+  for (int s = 0; s < p.nseg; ++s) total += p.seg[s].n;
+  const int64_t want = (total + 16384 - 1) / 16384;  // small problems: fewer CTAs
+  const int grid = (int)std::max<int64_t>(
+      1, std::min<int64_t>({(int64_t)di.sm_count * std::min(CPS, occ), want, (int64_t)kMaxGrid}));
+  const int N = p.seg_vec_elems;
+  for (int s = 0; s < p.nseg; ++s) {
+    Seg& sg = p.seg[s];
+    sg.nv = sg.vec ? (sg.n - sg.head) / N : 0;
+    sg.per = (sg.nv + grid - 1) / grid;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(AT + BT);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // CTAs wait on each other's partials
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  B2_CHECK(cudaLaunchKernelEx(&cfg, kern, p));
+  return B2_OK;
+}
+
 constexpr int kRingPieces = 13;  // 13 x 16 KB = 208 KB ring (+ barriers) per SM
 constexpr int kPiece = 16384;
 
@@ -763,20 +1024,23 @@ static int clip_cfg() {
   return v;
 }
 
-// K1 configuration: THREADS x CTAs/SM, lag, stream-A / stream-B loads in
-// flight per thread (tools/clip_bench.py sweeps; measurements in DESIGN.md).
-// B2_CLIP_CFG=5 selects the TMA-ring variant for A/B comparisons.
+// K1 configuration (tools/clip_bench.py sweeps; measurements in DESIGN.md):
+// several buckets per launch -> warp-specialised two-stream kernel
+// (256 norm + 256 scale threads, 2 CTAs/SM); a lone bucket (DDP-hook shape)
+// -> the time-sliced L2-lag kernel, which has the shorter critical path.
+// B2_CLIP_CFG overrides for A/B runs (5 = TMA ring, 10 = L2-lag, 20.. = ws).
 template <typename Tin, typename Tout>
 int launch_clip_k1(ClipParams& p, cudaStream_t stream) {
   if constexpr (std::is_same<Tin, float>::value && std::is_same<Tout, __nv_bfloat16>::value) {
     switch (clip_cfg()) {
       case 5: return launch_clip_tma_lag<Tin, Tout, 1, 0>(p, stream);
-      case 8: return launch_l2lag<Tin, Tout, 256, 3, 1, 8, 4, 0>(p, stream);
-      case 9: return launch_l2lag<Tin, Tout, 512, 2, 1, 4, 4, 0>(p, stream);
-      case 11: return launch_l2lag<Tin, Tout, 384, 2, 1, 8, 2, 0>(p, stream);
+      case 10: return launch_l2lag<Tin, Tout, 384, 2, 1, 8, 4, 0>(p, stream);
+      case 20: return launch_ws<Tin, Tout, 256, 256, 2, 1, 8, 4>(p, stream);
+      case 24: return launch_ws<Tin, Tout, 128, 128, 4, 1, 8, 4>(p, stream);
       default: break;
     }
   }
+  if (p.nseg >= 2) return launch_ws<Tin, Tout, 256, 256, 2, 1, 8, 4>(p, stream);
   return launch_l2lag<Tin, Tout, 384, 2, 1, 8, 4, 0>(p, stream);
 }
 
