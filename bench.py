@@ -176,19 +176,33 @@ def bench_clip(args, rank, world, local):
         mode = "one fused K1 launch over all 52 buckets (no allreduce at N=1)"
         launches_per_step = 1
     else:
-        # per-bucket K1 on the compute stream, NCCL average of the bf16 bucket on a side stream
-        per_bucket = [clip.prepare(g, comm, [s], limit) for s in segs]
+        # native step: per bucket (backward order) K1 on the compute stream, then
+        # ncclAllReduce(avg, bf16) of that bucket on a side stream — one C call,
+        # captured once into a CUDA graph
+        bsync = BucketwiseSync(layout, cfg, comm_dtype=torch.bfloat16)
 
-        def step():
-            for i, b in enumerate(order):
-                a, e = layout[b]
-                per_bucket[i]()
-                evs[b].record(compute)
-                side.wait_event(evs[b])
-                with torch.cuda.stream(side):
-                    dist.all_reduce(comm[a:e], op=dist.ReduceOp.AVG)
-            compute.wait_stream(side)
-        mode = "per-bucket K1 + ncclAllReduce(avg, bf16) per bucket on a side stream"
+        def step_eager(stream=None):
+            s_ = stream if stream is not None else compute
+            bsync.sync_native(g, stream=s_)
+            s_.wait_stream(bsync.side)
+
+        step = step_eager
+        mode = "per-bucket K1 + ncclAllReduce(avg, bf16) per bucket on a side stream (native, eager)"
+        try:
+            cap = torch.cuda.Stream()
+            cap.wait_stream(compute)
+            with torch.cuda.stream(cap):
+                step_eager(cap)
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=cap):
+                step_eager(cap)
+            torch.cuda.synchronize()
+            step = graph.replay
+            mode = "per-bucket K1 + ncclAllReduce(avg, bf16) per bucket on a side stream (native, CUDA graph)"
+        except Exception as e:  # capture unsupported: stay eager, say so
+            mode += f"; graph capture failed: {str(e)[:120]}"
+            torch.cuda.synchronize()
         launches_per_step = nb
 
     for _ in range(args.warmup):
@@ -270,9 +284,26 @@ def bench_clip(args, rank, world, local):
     }
     if world > 1:
         algbw = dim * 2 / (ms * 1e-3) / 1e9
-        res["nvlink"] = {"algbw_gbs": algbw, "busbw_gbs": algbw * 2 * (world - 1) / world,
-                         "peak_gbs": 900.0, "busbw_frac": algbw * 2 * (world - 1) / world / 900.0,
-                         "comm_dtype": "bf16", "collective": "ncclAllReduce avg per bucket, side stream"}
+        # NCCL alone on the same 52 bf16 buckets (no clip) = the comm floor of the step
+        for _ in range(3):
+            for b in order:
+                bsync.nccl.all_reduce_avg(bsync.comm[layout[b][0]:layout[b][1]], compute)
+        torch.cuda.synchronize()
+        barrier(world)
+        k0.record(compute)
+        for _ in range(args.steps):
+            for b in order:
+                bsync.nccl.all_reduce_avg(bsync.comm[layout[b][0]:layout[b][1]], compute)
+        k1.record(compute)
+        torch.cuda.synchronize()
+        nccl_ms = max_over_ranks(k0.elapsed_time(k1) / args.steps, world)
+        nccl_algbw = dim * 2 / (nccl_ms * 1e-3) / 1e9
+        bus = lambda a: a * 2 * (world - 1) / world
+        res["nvlink"] = {"algbw_gbs": algbw, "busbw_gbs": bus(algbw), "peak_gbs": 900.0,
+                         "busbw_frac": bus(algbw) / 900.0, "peak_measured_gbs": 770.0,
+                         "nccl_only_ms": nccl_ms, "nccl_only_busbw_gbs": bus(nccl_algbw),
+                         "clip_hidden_frac": min(1.0, nccl_ms / ms),
+                         "comm_dtype": "bf16", "collective": "ncclAllReduce avg per 25 MiB bucket, side stream"}
 
     # e2e: pinned host fp32 gradients -> device -> sync -> host result, through the public API
     host = torch.empty((1, dim), dtype=torch.float32, pin_memory=True)

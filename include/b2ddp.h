@@ -91,6 +91,35 @@ int b2_weighted_mean(const void* G, int in_dtype, int64_t K, int64_t D, int64_t 
                      int out_dtype, void* stream);
 
 /* ------------------------------------------------------------------------
+ * H1 across ranks (one process per GPU): NCCL, loaded at run time
+ * ---------------------------------------------------------------------- */
+
+typedef struct b2_comm b2_comm;
+
+/* 128-byte ncclUniqueId from rank 0 (distribute it with any side channel,
+ * e.g. the torch.distributed store).  libnccl_path may be NULL: the
+ * libnccl.so.2 already loaded in the process (torch's) is used. */
+int b2_nccl_unique_id(void* uid128, const char* libnccl_path);
+int b2_comm_create(b2_comm** comm, int nranks, int rank, const void* uid128, const char* libnccl_path);
+int b2_comm_destroy(b2_comm* comm);
+
+/* In-place ncclAllReduce(avg) of n elements (B2_F32 | B2_BF16 | B2_F64). */
+int b2_allreduce_avg(b2_comm* comm, void* buf, int64_t n, int dtype, void* stream);
+
+/* One H1 step (sync_bucketwise, gradsync.py:148-162, rank r = worker row r):
+ * for every bucket s in the given order (pass them reversed, :157): K1 clips
+ * in[seg_off[s] .. +seg_len[s]) at `limit` into out at the same offset on
+ * `stream`, an event chains `comm_stream` after it, and ncclAllReduce(avg)
+ * reduces that bucket of `out` on `comm_stream` — bucket s's transfer
+ * overlaps the clip of s+1.  The caller joins comm_stream before reading
+ * `out`.  `norms`/`nonfinite` (device, nseg entries) are optional.  Graph
+ * capturable. */
+int b2_bucket_clip_allreduce(b2_comm* comm, const void* in, int in_dtype, void* out, int out_dtype,
+                             const int64_t* seg_off, const int64_t* seg_len, int nseg, double limit,
+                             double* norms, int32_t* nonfinite, void* workspace, size_t workspace_bytes,
+                             void* stream, void* comm_stream);
+
+/* ------------------------------------------------------------------------
  * H2 — stratified local presort
  * ---------------------------------------------------------------------- */
 

@@ -28,6 +28,14 @@ SIGNATURES = {
         [_P, _I, _P, _I, _P, _P, _P, _I, _D, _D, _P, _P, _P, _P, _SZ, _I, _P],
     ),
     "b2_weighted_mean": (_I, [_P, _I, _I64, _I64, _I64, _P, _P, _I, _P, _I, _P]),
+    "b2_nccl_unique_id": (_I, [_P, C.c_char_p]),
+    "b2_comm_create": (_I, [C.POINTER(C.c_void_p), _I, _I, _P, C.c_char_p]),
+    "b2_comm_destroy": (_I, [_P]),
+    "b2_allreduce_avg": (_I, [_P, _P, _I64, _I, _P]),
+    "b2_bucket_clip_allreduce": (
+        _I,
+        [_P, _P, _I, _P, _I, _P, _P, _I, _D, _P, _P, _P, _SZ, _P, _P],
+    ),
     "b2_strata_workspace_bytes": (_SZ, [_I64]),
     "b2_strata_partition": (_I, [_P, _P, _I64, _P, _I, _P, _P, _P, _P, _SZ, _P]),
     "b2_presort_deal": (

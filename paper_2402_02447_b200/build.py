@@ -9,12 +9,12 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
-SOURCES = ["capi.cu", "bucket_clip.cu", "strata.cu", "presort.cu"]
+SOURCES = ["capi.cu", "bucket_clip.cu", "comm.cu", "strata.cu", "presort.cu"]
 OUT = PKG / "_native" / "libb2ddp.so"
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC", "-shared", "-ldl",
 ]
 
 

@@ -17,13 +17,59 @@ overlaps the clip (and, in training, the backward) of bucket b-1.
 
 from __future__ import annotations
 
+import ctypes
 import math
 from typing import Sequence
 
 import torch
 import torch.distributed as dist
 
-from .gradsync import BucketClipper, ClipConfig, ClipMode
+from . import _lib
+from .gradsync import _DT, BucketClipper, ClipConfig, ClipMode
+
+
+def _libnccl_path() -> bytes:
+    try:
+        import nvidia.nccl
+
+        from pathlib import Path
+
+        return str(Path(list(nvidia.nccl.__path__)[0]) / "lib" / "libnccl.so.2").encode()
+    except ImportError:
+        return b""
+
+
+class NcclComm:
+    """An NCCL communicator owned by libb2ddp, bootstrapped over a torch.distributed group.
+
+    The native H1 step (b2_bucket_clip_allreduce) issues K1 and ncclAllReduce
+    for all buckets from C, so per-bucket cost is a kernel launch, not a
+    Python/c10d round trip.
+    """
+
+    def __init__(self, group=None):
+        self.lib = _lib.load()
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        uid = (ctypes.c_char * 128)()
+        path = _libnccl_path()
+        if self.rank == 0:
+            _lib.check(self.lib.b2_nccl_unique_id(uid, path))
+        obj = [bytes(uid)]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        uid = (ctypes.c_char * 128).from_buffer_copy(obj[0])
+        handle = ctypes.c_void_p()
+        _lib.check(self.lib.b2_comm_create(ctypes.byref(handle), self.world, self.rank, uid, path))
+        self.handle = handle
+
+    def all_reduce_avg(self, buf: torch.Tensor, stream=None) -> None:
+        _lib.check(self.lib.b2_allreduce_avg(self.handle, buf.data_ptr(), buf.numel(), _DT[buf.dtype],
+                                             _lib.stream_ptr(stream)))
+
+    def close(self) -> None:
+        if self.handle:
+            _lib.check(self.lib.b2_comm_destroy(self.handle))
+            self.handle = None
 
 
 def _avg_op(group) -> tuple:
@@ -45,7 +91,7 @@ class BucketwiseSync:
     """
 
     def __init__(self, layout: Sequence, cfg: ClipConfig, comm_dtype=torch.bfloat16, group=None,
-                 device=None, clip=None, ctas_per_sm: int = 0):
+                 device=None, clip=None, ctas_per_sm: int = 0, native: bool | None = None):
         if ClipConfig(cfg.threshold, cfg.mode).mode is not ClipMode.BUCKET_WISE:
             raise ValueError(f"config mode is {cfg.mode.value}, expected {ClipMode.BUCKET_WISE.value}")
         self.layout = tuple((int(a), int(b)) for a, b in layout)
@@ -61,9 +107,34 @@ class BucketwiseSync:
             self.compute = torch.cuda.current_stream(self.device)
             self.side = torch.cuda.Stream(device=self.device)
             self.events = [torch.cuda.Event() for _ in self.layout]
-        self.clip = clip if clip is not None else BucketClipper(device=self.device, ctas_per_sm=ctas_per_sm).clip_cast
+        self.clipper = None if clip is not None else BucketClipper(device=self.device, ctas_per_sm=ctas_per_sm)
+        self.clip = clip if clip is not None else self.clipper.clip_cast
         self.norms = torch.zeros(len(self.layout), dtype=torch.float64, device=self.device)
         self.works: list = []
+        # native path: whole step in one C call (K1 + ncclAllReduce per bucket)
+        if native is None:
+            native = self.is_cuda and clip is None and dist.get_backend(group) == "nccl"
+        self.native = bool(native)
+        if self.native:
+            self.nccl = NcclComm(group)
+            order = list(reversed(range(len(self.layout))))
+            self._offs = _lib.i64_array(self.layout[b][0] for b in order)
+            self._lens = _lib.i64_array(self.layout[b][1] - self.layout[b][0] for b in order)
+            self._norms_call = torch.zeros(len(self.layout), dtype=torch.float64, device=self.device)
+            self._pending = False
+
+    def sync_native(self, grad: torch.Tensor, stream=None) -> torch.Tensor:
+        """One C call: per bucket (backward order) K1 on `stream`, ncclAllReduce(avg) on the side stream."""
+        lib = self.clipper.lib
+        ws = self.clipper.workspace
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self.side.wait_stream(s)  # the comm stream must not run ahead of the previous step's readers
+        _lib.check(lib.b2_bucket_clip_allreduce(
+            self.nccl.handle, grad.data_ptr(), _DT[grad.dtype], self.comm.data_ptr(), _DT[self.comm.dtype],
+            self._offs, self._lens, len(self.layout), float(self.limit), self._norms_call.data_ptr(), None,
+            ws.data_ptr(), ws.numel(), int(s.cuda_stream), int(self.side.cuda_stream)))
+        self._pending = True
+        return self.comm
 
     def launch_bucket(self, grad: torch.Tensor, b: int) -> None:
         """K1 for bucket b on the compute stream, then its allreduce on the side stream."""
@@ -82,6 +153,10 @@ class BucketwiseSync:
         """All buckets in backward order; returns the averaged comm buffer (not yet waited)."""
         if grad.numel() != self.dim:
             raise ValueError(f"gradient has {grad.numel()} elements, layout covers {self.dim}")
+        if self.native:
+            if self.clipper.stream is not None:
+                raise ValueError("native sync runs on the current stream")
+            return self.sync_native(grad)
         for b in reversed(range(len(self.layout))):
             self.launch_bucket(grad, b)
         return self.comm
@@ -93,13 +168,17 @@ class BucketwiseSync:
         self.works.clear()
         if self.is_cuda:
             torch.cuda.current_stream(self.device).wait_stream(self.side)
+        if self.native and self._pending:
+            self.norms.copy_(self._norms_call.flip(0))  # call order is reversed bucket order
+            self._pending = False
         return self.comm
 
 
 class _HookState:
-    def __init__(self, cfg: ClipConfig, num_buckets: int, process_group=None):
+    def __init__(self, cfg: ClipConfig, num_buckets: int, process_group=None, clip=None):
         self.limit = cfg.threshold / math.sqrt(num_buckets)
         self.group = process_group
+        self.clip = clip  # optional replacement of BucketClipper.clip_cast (CPU tests)
         self.clipper = None
         self.norms = {}
 
@@ -112,18 +191,21 @@ def bucketwise_clip_hook(state: _HookState, bucket):
     parameter sizes), because the threshold is c/sqrt(B) (gradsync.py:155).
     """
     buf = bucket.buffer()
-    if state.clipper is None:
-        state.clipper = BucketClipper(device=buf.device)
+    clip = state.clip
+    if clip is None:
+        if state.clipper is None:
+            state.clipper = BucketClipper(device=buf.device)
+        clip = state.clipper.clip_cast
     op, post = _avg_op(state.group)
     n = buf.numel()
     norm = torch.empty(1, dtype=torch.float64, device=buf.device)
-    state.clipper.clip_cast(buf, buf, [(0, 0, n)], state.limit, post, norms=norm)  # in place
+    clip(buf, buf, [(0, 0, n)], state.limit, post, norm)  # in place: K1 reads before it writes
     state.norms[bucket.index()] = norm
     fut = dist.all_reduce(buf, op=op, group=state.group, async_op=True).get_future()
     return fut.then(lambda f: f.value()[0])
 
 
-def make_hook_state(cfg: ClipConfig, num_buckets: int, process_group=None) -> _HookState:
+def make_hook_state(cfg: ClipConfig, num_buckets: int, process_group=None, clip=None) -> _HookState:
     if ClipConfig(cfg.threshold, cfg.mode).mode is not ClipMode.BUCKET_WISE:
         raise ValueError(f"config mode is {cfg.mode.value}, expected {ClipMode.BUCKET_WISE.value}")
-    return _HookState(cfg, num_buckets, process_group)
+    return _HookState(cfg, num_buckets, process_group, clip)

@@ -1,0 +1,111 @@
+"""H1 over NCCL on >= 2 GPUs: per-bucket K1 + ncclAllReduce(avg) == reference semantics.
+
+Skipped on single-GPU boxes; run with `gpurun --gpus 2`.
+"""
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+from tests import dist_helpers as H
+
+pytestmark = pytest.mark.gpu
+
+DIM = 20_000_003
+LAYOUT = ((0, 6_553_600), (6_553_600, 13_107_200), (13_107_200, 19_660_800), (19_660_800, DIM))
+
+
+def _world():
+    return min(torch.cuda.device_count(), 4)
+
+
+def _sync_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    from paper_2402_02447_b200 import ClipConfig
+    from paper_2402_02447_b200.ddp import BucketwiseSync
+
+    H.init(rank, world, port, "nccl")
+    try:
+        g = H.worker_grad(rank, DIM).cuda()
+        res = {}
+        for dt in (torch.float32, torch.bfloat16):
+            sync = BucketwiseSync(LAYOUT, ClipConfig(1.0, "bucket_wise"), comm_dtype=dt)
+            sync.sync(g)
+            res[str(dt)] = sync.wait().float().cpu().numpy()
+            res["norms"] = sync.norms.cpu().numpy()
+        torch.cuda.synchronize()
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def _hook_worker(rank, world, port, q):
+    import torch.distributed as dist
+    from torch.nn.parallel import DistributedDataParallel as DDP
+
+    from paper_2402_02447_b200 import ClipConfig
+    from paper_2402_02447_b200.ddp import bucketwise_clip_hook, make_hook_state
+
+    H.init(rank, world, port, "nccl")
+    try:
+        torch.manual_seed(0)
+        model = torch.nn.Sequential(torch.nn.Linear(256, 512), torch.nn.Tanh(), torch.nn.Linear(512, 64)).cuda()
+        ref_model = torch.nn.Sequential(torch.nn.Linear(256, 512), torch.nn.Tanh(), torch.nn.Linear(512, 64)).cuda()
+        ref_model.load_state_dict(model.state_dict())
+        ddp = DDP(model, device_ids=[rank], bucket_cap_mb=100)  # one bucket: B = 1
+        ddp.register_comm_hook(make_hook_state(ClipConfig(0.5, "bucket_wise"), 1), bucketwise_clip_hook)
+        torch.manual_seed(10 + rank)
+        x = torch.randn(32, 256, device="cuda") * (1.0 + 10.0 * rank)
+        ddp(x).pow(2).sum().backward()
+        ref_model(x).pow(2).sum().backward()
+        raw = torch.cat([p.grad.reshape(-1) for p in ref_model.parameters()]).cpu().numpy()
+        synced = torch.cat([p.grad.reshape(-1) for p in model.parameters()]).cpu().numpy()
+        q.put((rank, {"raw": raw, "synced": synced}))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(target, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = H.free_port()
+    procs = [ctx.Process(target=target, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return res
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_bucketwise_sync_nccl_matches_reference():
+    from oracle import ddp_oracle as O
+
+    world = _world()
+    res = _run(_sync_worker, world)
+    W = np.stack([H.worker_grad(r, DIM).double().numpy() for r in range(world)])
+    ref = O.sync_bucketwise(W, LAYOUT, 1.0)
+    scale = np.abs(ref).max()
+    for r in range(world):
+        out32 = res[r][str(torch.float32)]
+        assert np.abs(out32 - ref).max() <= 1e-5 * scale  # fp32 comm buffer: the 1e-5 contract
+        out16 = res[r][str(torch.bfloat16)]
+        assert np.abs(out16 - ref).max() <= 2.0 ** -7 * scale  # bf16 comm + bf16 NCCL sum
+        rn = np.array([np.linalg.norm(W[r, a:b]) for a, b in LAYOUT])
+        np.testing.assert_allclose(res[r]["norms"], rn, rtol=1e-6)
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_ddp_comm_hook_nccl():
+    from oracle import ddp_oracle as O
+
+    world = _world()
+    res = _run(_hook_worker, world)
+    raws = np.stack([res[r]["raw"].astype(np.float64) for r in range(world)])
+    ref = O.sync_before(raws, 0.5)
+    for r in range(world):
+        assert np.abs(res[r]["synced"] - ref).max() <= 1e-5 * np.abs(ref).max()
