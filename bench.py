@@ -176,35 +176,49 @@ def bench_clip(args, rank, world, local):
         mode = "one fused K1 launch over all 52 buckets (no allreduce at N=1)"
         launches_per_step = 1
     else:
-        # native step: per bucket (backward order) K1 on the compute stream, then
-        # ncclAllReduce(avg, bf16) of that bucket on a side stream — one C call,
-        # captured once into a CUDA graph
+        from paper_2402_02447_b200.ddp import FusedBucketSync
+
+        def capture(fn):
+            """Capture fn(stream) once into a CUDA graph; return (replay, note)."""
+            try:
+                cap = torch.cuda.Stream()
+                cap.wait_stream(compute)
+                with torch.cuda.stream(cap):
+                    fn(cap)
+                torch.cuda.synchronize()
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph, stream=cap):
+                    fn(cap)
+                torch.cuda.synchronize()
+                return graph.replay, "CUDA graph"
+            except Exception as e:  # capture unsupported: stay eager, say so
+                torch.cuda.synchronize()
+                return (lambda: fn(compute)), f"eager (graph capture failed: {str(e)[:100]})"
+
+        # (a) NCCL path: per bucket K1 on the compute stream + ncclAllReduce(avg, bf16) on a side stream
         bsync = BucketwiseSync(layout, cfg, comm_dtype=torch.bfloat16)
 
-        def step_eager(stream=None):
-            s_ = stream if stream is not None else compute
+        def nccl_step(s_):
             bsync.sync_native(g, stream=s_)
             s_.wait_stream(bsync.side)
 
-        step = step_eager
-        mode = "per-bucket K1 + ncclAllReduce(avg, bf16) per bucket on a side stream (native, eager)"
-        try:
-            cap = torch.cuda.Stream()
-            cap.wait_stream(compute)
-            with torch.cuda.stream(cap):
-                step_eager(cap)
-            torch.cuda.synchronize()
-            graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph, stream=cap):
-                step_eager(cap)
-            torch.cuda.synchronize()
-            step = graph.replay
-            mode = "per-bucket K1 + ncclAllReduce(avg, bf16) per bucket on a side stream (native, CUDA graph)"
-        except Exception as e:  # capture unsupported: stay eager, say so
-            mode += f"; graph capture failed: {str(e)[:120]}"
-            torch.cuda.synchronize()
-        launches_per_step = nb
-
+        nccl_replay, nccl_note = capture(nccl_step)
+        # (b) fused path: one kernel per rank clips and reduces every bucket over NVLink peer memory
+        fused_replay, fused_note = None, "unavailable"
+        if args.comm == "fused":
+            try:
+                fsync = FusedBucketSync(layout, cfg)
+                fused_replay, fused_note = capture(lambda s_: fsync.sync(g, stream=s_))
+            except Exception as e:
+                fused_note = f"unavailable: {str(e)[:120]}"
+        if fused_replay is not None:
+            step = fused_replay
+            mode = f"fused K1 + two-shot NVLink allreduce per bucket, one kernel per rank ({fused_note})"
+            launches_per_step = 1
+        else:
+            step = nccl_replay
+            mode = f"per-bucket K1 + ncclAllReduce(avg, bf16) on a side stream ({nccl_note}); fused: {fused_note}"
+            launches_per_step = nb
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -298,12 +312,24 @@ def bench_clip(args, rank, world, local):
         torch.cuda.synchronize()
         nccl_ms = max_over_ranks(k0.elapsed_time(k1) / args.steps, world)
         nccl_algbw = dim * 2 / (nccl_ms * 1e-3) / 1e9
+        for _ in range(3):
+            nccl_replay()
+        torch.cuda.synchronize()
+        barrier(world)
+        k0.record(compute)
+        for _ in range(args.steps):
+            nccl_replay()
+        k1.record(compute)
+        torch.cuda.synchronize()
+        nccl_step_ms = max_over_ranks(k0.elapsed_time(k1) / args.steps, world)
         bus = lambda a: a * 2 * (world - 1) / world
         res["nvlink"] = {"algbw_gbs": algbw, "busbw_gbs": bus(algbw), "peak_gbs": 900.0,
                          "busbw_frac": bus(algbw) / 900.0, "peak_measured_gbs": 770.0,
                          "nccl_only_ms": nccl_ms, "nccl_only_busbw_gbs": bus(nccl_algbw),
-                         "clip_hidden_frac": min(1.0, nccl_ms / ms),
-                         "comm_dtype": "bf16", "collective": "ncclAllReduce avg per 25 MiB bucket, side stream"}
+                         "nccl_step_ms": nccl_step_ms, "speedup_vs_nccl_step": nccl_step_ms / ms,
+                         "comm_dtype": "bf16",
+                         "collective": "fused two-shot over CUDA-IPC peer memory" if launches_per_step == 1
+                         else "ncclAllReduce avg per 25 MiB bucket, side stream"}
 
     # e2e: pinned host fp32 gradients -> device -> sync -> host result, through the public API
     host = torch.empty((1, dim), dtype=torch.float32, pin_memory=True)
@@ -316,17 +342,23 @@ def bench_clip(args, rank, world, local):
         d2h = dim * 4
         api = "GradientState + sync_bucketwise (pinned host fp32 in, host fp32 out)"
     else:
-        sync = BucketwiseSync(layout, cfg, comm_dtype=torch.bfloat16)
         out_host = torch.empty(dim, dtype=torch.bfloat16, pin_memory=True)
-
-        def e2e_step():
-            dg = host.view(-1).to("cuda", non_blocking=True)
-            sync.sync(dg)
-            out_host.copy_(sync.wait(), non_blocking=True)
-            torch.cuda.current_stream().synchronize()
-            return out_host
+        if launches_per_step == 1:
+            def e2e_step():
+                dg = host.view(-1).to("cuda", non_blocking=True)
+                out_host.copy_(fsync.sync(dg), non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+                return out_host
+            api = "FusedBucketSync.sync (pinned host fp32 in, host bf16 out)"
+        else:
+            def e2e_step():
+                dg = host.view(-1).to("cuda", non_blocking=True)
+                bsync.sync(dg)
+                out_host.copy_(bsync.wait(), non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+                return out_host
+            api = "BucketwiseSync.sync (pinned host fp32 in, host bf16 out)"
         d2h = dim * 2
-        api = "BucketwiseSync.sync (pinned host fp32 in, host bf16 out)"
     e2e_step()
     torch.cuda.synchronize()
     barrier(world)
@@ -520,6 +552,8 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-presort", action="store_true")
+    ap.add_argument("--comm", choices=("fused", "nccl"), default="fused",
+                    help="N>1: fused clip+NVLink allreduce kernel (default) or per-bucket NCCL")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 

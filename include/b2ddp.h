@@ -119,6 +119,27 @@ int b2_bucket_clip_allreduce(b2_comm* comm, const void* in, int in_dtype, void* 
                              double* norms, int32_t* nonfinite, void* workspace, size_t workspace_bytes,
                              void* stream, void* comm_stream);
 
+/* Fused H1 step over NVLink peer memory (no NCCL): ONE persistent kernel per
+ * rank computes each bucket's norm, clips + casts it to bf16 into this rank's
+ * symmetric stage buffer, and runs a two-shot allreduce of the bucket (this
+ * rank reduces its 1/N slice from every stage, writes the mean into every
+ * stage).  stages[q] / flags[q] ([host] arrays of nranks device pointers) are
+ * rank q's bf16 stage (D elements, buckets at seg_off) and its flag area
+ * (b2_p2p_flag_bytes(), zeroed once) as mapped in this process (b2_ipc_*).
+ * On return of the launch (stream order) stages[rank] holds the averaged,
+ * clipped gradient.  All ranks must issue the same calls in the same order;
+ * cross-GPU waits trap after 30 s.  nranks <= 8, nseg <= 128, buckets
+ * 8-element aligned.  The workspace (b2_clip_workspace_bytes) also carries
+ * the launch epoch, so the call is CUDA-graph replayable. */
+size_t b2_p2p_flag_bytes(void);
+int b2_ipc_export(const void* dev_ptr, void* handle64, int64_t* offset);
+int b2_ipc_import(const void* handle64, int64_t offset, void** base, void** dev_ptr);
+int b2_ipc_close(void* base);
+int b2_bucket_clip_allreduce_p2p(const void* in, void* const* stages, uint32_t* const* flags, int nranks, int rank,
+                                 const int64_t* seg_off, const int64_t* seg_len, int nseg, double limit,
+                                 double* norms, int32_t* nonfinite, void* workspace, size_t workspace_bytes,
+                                 void* stream);
+
 /* ------------------------------------------------------------------------
  * H2 — stratified local presort
  * ---------------------------------------------------------------------- */

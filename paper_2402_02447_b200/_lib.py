@@ -36,6 +36,14 @@ SIGNATURES = {
         _I,
         [_P, _P, _I, _P, _I, _P, _P, _I, _D, _P, _P, _P, _SZ, _P, _P],
     ),
+    "b2_p2p_flag_bytes": (_SZ, []),
+    "b2_ipc_export": (_I, [_P, _P, C.POINTER(C.c_int64)]),
+    "b2_ipc_import": (_I, [_P, _I64, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
+    "b2_ipc_close": (_I, [_P]),
+    "b2_bucket_clip_allreduce_p2p": (
+        _I,
+        [_P, _P, _P, _I, _I, _P, _P, _I, _D, _P, _P, _P, _SZ, _P],
+    ),
     "b2_strata_workspace_bytes": (_SZ, [_I64]),
     "b2_strata_partition": (_I, [_P, _P, _I64, _P, _I, _P, _P, _P, _P, _SZ, _P]),
     "b2_presort_deal": (

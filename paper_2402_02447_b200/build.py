@@ -9,7 +9,7 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
-SOURCES = ["capi.cu", "bucket_clip.cu", "comm.cu", "strata.cu", "presort.cu"]
+SOURCES = ["capi.cu", "bucket_clip.cu", "fused_allreduce.cu", "comm.cu", "strata.cu", "presort.cu"]
 OUT = PKG / "_native" / "libb2ddp.so"
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -27,7 +27,7 @@ def nvcc() -> str:
 
 def build(verbose: bool = False) -> Path:
     srcs = [PKG / "csrc" / s for s in SOURCES]
-    deps = srcs + [PKG / "csrc" / "common.cuh", ROOT / "include" / "b2ddp.h"]
+    deps = srcs + list((PKG / "csrc").glob("*.cuh")) + [ROOT / "include" / "b2ddp.h"]
     if OUT.exists() and all(OUT.stat().st_mtime >= d.stat().st_mtime for d in deps):
         return OUT
     OUT.parent.mkdir(parents=True, exist_ok=True)

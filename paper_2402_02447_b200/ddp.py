@@ -209,3 +209,85 @@ def make_hook_state(cfg: ClipConfig, num_buckets: int, process_group=None, clip=
     if ClipConfig(cfg.threshold, cfg.mode).mode is not ClipMode.BUCKET_WISE:
         raise ValueError(f"config mode is {cfg.mode.value}, expected {ClipMode.BUCKET_WISE.value}")
     return _HookState(cfg, num_buckets, process_group, clip)
+
+
+class FusedBucketSync:
+    """Bucket-wise clip + allreduce fused in one kernel per rank, over NVLink peer memory.
+
+    Same contract as ``BucketwiseSync`` (rank r = worker row r, sync_bucketwise
+    semantics, gradsync.py:148-162) with a bf16 comm buffer, but no NCCL: the
+    clip kernel itself reduces each bucket as soon as every rank has staged it
+    (two-shot over CUDA-IPC-mapped peer buffers; b2_bucket_clip_allreduce_p2p).
+    ``sync(grad)`` returns ``self.stage``, which holds the averaged clipped
+    gradient once the launch completes in stream order (graph-replayable).
+    """
+
+    def __init__(self, layout: Sequence, cfg: ClipConfig, group=None, device=None):
+        if ClipConfig(cfg.threshold, cfg.mode).mode is not ClipMode.BUCKET_WISE:
+            raise ValueError(f"config mode is {cfg.mode.value}, expected {ClipMode.BUCKET_WISE.value}")
+        self.lib = _lib.load()
+        self.layout = tuple((int(a), int(b)) for a, b in layout)
+        if len(self.layout) > 128:
+            raise ValueError("fused sync supports at most 128 buckets per step")
+        if any(a % 8 or (b - a) % 8 for a, b in self.layout):
+            raise ValueError("fused sync needs 8-element aligned buckets")
+        self.limit = cfg.threshold / math.sqrt(len(self.layout))  # gradsync.py:155
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        if self.world > 8:
+            raise ValueError("fused sync supports up to 8 ranks")
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.dim = self.layout[-1][1]
+        stage_bytes = (self.dim * 2 + 255) // 256 * 256
+        flag_bytes = self.lib.b2_p2p_flag_bytes()
+        self.buf = torch.zeros(stage_bytes + flag_bytes, dtype=torch.uint8, device=self.device)
+        self.stage = self.buf[: self.dim * 2].view(torch.bfloat16)
+        handle = (ctypes.c_char * 64)()
+        off = ctypes.c_int64()
+        _lib.check(self.lib.b2_ipc_export(self.buf.data_ptr(), handle, ctypes.byref(off)))
+        peers = [None] * self.world
+        dist.all_gather_object(peers, (bytes(handle), off.value), group=group)
+        self._opened = []
+        stages, flags = [], []
+        for q, (h, o) in enumerate(peers):
+            if q == self.rank:
+                ptr = self.buf.data_ptr()
+            else:
+                base, p = ctypes.c_void_p(), ctypes.c_void_p()
+                hb = (ctypes.c_char * 64).from_buffer_copy(h)
+                _lib.check(self.lib.b2_ipc_import(hb, o, ctypes.byref(base), ctypes.byref(p)))
+                self._opened.append(base)
+                ptr = p.value
+            stages.append(ptr)
+            flags.append(ptr + stage_bytes)
+        self._stages = (ctypes.c_void_p * self.world)(*stages)
+        self._flags = (ctypes.c_void_p * self.world)(*flags)
+        self.clipper = BucketClipper(device=self.device)
+        order = list(reversed(range(len(self.layout))))  # backward order (:157)
+        self._offs = _lib.i64_array(self.layout[b][0] for b in order)
+        self._lens = _lib.i64_array(self.layout[b][1] - self.layout[b][0] for b in order)
+        self._norms_call = torch.zeros(len(self.layout), dtype=torch.float64, device=self.device)
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=group)
+
+    def sync(self, grad: torch.Tensor, stream=None) -> torch.Tensor:
+        if grad.numel() != self.dim or grad.dtype != torch.float32 or not grad.is_cuda:
+            raise ValueError(f"expected a CUDA float32 gradient of {self.dim} elements")
+        ws = self.clipper.workspace
+        _lib.check(self.lib.b2_bucket_clip_allreduce_p2p(
+            grad.data_ptr(), self._stages, self._flags, self.world, self.rank, self._offs, self._lens,
+            len(self.layout), float(self.limit), self._norms_call.data_ptr(), None, ws.data_ptr(), ws.numel(),
+            _lib.stream_ptr(stream)))
+        return self.stage
+
+    @property
+    def norms(self) -> torch.Tensor:
+        """This rank's per-bucket norms, in layout order."""
+        return self._norms_call.flip(0)
+
+    def close(self) -> None:
+        torch.cuda.synchronize(self.device)
+        for base in self._opened:
+            _lib.check(self.lib.b2_ipc_close(base))
+        self._opened.clear()
