@@ -410,20 +410,20 @@ def bench_presort(args):
     lib = _lib.load()
     shard = CORPUS_N // SHARDS
     d_lens = torch.from_numpy(lens).cuda()
-    ws_bytes = lib.b2_strata_workspace_bytes(shard)
-    wss = [torch.empty(ws_bytes, dtype=torch.uint8, device="cuda") for _ in range(SHARDS)]
+    ws_bytes = lib.b2_strata_workspace_bytes(CORPUS_N)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
     ids_out = torch.empty(CORPUS_N, dtype=torch.int32, device="cuda")
     counts = torch.empty((SHARDS, 4), dtype=torch.int64, device="cuda")
     bad = torch.empty(SHARDS, dtype=torch.int64, device="cuda")
     bnds = _lib.i32_array(BOUNDS)
+    offs = _lib.i64_array(r * shard for r in range(SHARDS + 1))
     sp = _lib.stream_ptr()
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
-    def k2():
-        for r in range(SHARDS):
-            _lib.check(lib.b2_strata_partition(
-                d_lens[r * shard:].data_ptr(), None, shard, bnds, 4, ids_out[r * shard:].data_ptr(),
-                counts[r].data_ptr(), bad[r:].data_ptr(), wss[r].data_ptr(), ws_bytes, sp))
+    def k2():  # every rank shard stratified in one pass (2 launches)
+        _lib.check(lib.b2_strata_partition_shards(
+            d_lens.data_ptr(), None, offs, SHARDS, bnds, 4, ids_out.data_ptr(), counts.data_ptr(),
+            bad.data_ptr(), ws.data_ptr(), ws_bytes, sp))
 
     res = {}
     for lb in (16, 48):
@@ -460,7 +460,7 @@ def bench_presort(args):
             "keys_per_s": keys / ((t2 + t3) * 1e-3), "ms_per_step": t2 + t3, "node_steps": steps,
             "keys_presorted": keys, "keys_partitioned": CORPUS_N,
             "k2_partition": {"ms": t2, "achieved_gbs": k2_gbs, "frac": k2_gbs / hbm, "bytes_per_key": 8,
-                             "launches": SHARDS * 3},
+                             "launches": 2, "shards": SHARDS},
             "k3_presort_deal": {"ms": t3, "achieved_gbs": k3_gbs, "frac": k3_gbs / hbm, "bytes_per_key": 12,
                                 "launches": 1},
         }

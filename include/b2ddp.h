@@ -159,6 +159,16 @@ int b2_strata_partition(const int32_t* lengths, const int32_t* ids, int64_t n,
                         const int32_t* bounds, int nb, int32_t* ids_out, int64_t* counts,
                         int64_t* bad, void* workspace, size_t workspace_bytes, void* stream);
 
+/* K2 over many rank shards in one pass (two launches in total): shard g is
+ * lengths[shard_off[g] .. shard_off[g+1]) ([host] offsets, nshard <= 64) and
+ * is stratified on its own, exactly like stratify() on that shard; ids_out
+ * uses the same offsets, counts is [nshard][nb], bad[g] is the shard-local
+ * index of its first bad sample or -1.  ids NULL -> shard-local indices.
+ * Workspace: b2_strata_workspace_bytes(total samples). */
+int b2_strata_partition_shards(const int32_t* lengths, const int32_t* ids, const int64_t* shard_off, int nshard,
+                               const int32_t* bounds, int nb, int32_t* ids_out, int64_t* counts, int64_t* bad,
+                               void* workspace, size_t workspace_bytes, void* stream);
+
 /* K3 — per-pool stable sort by (-length, id) + raster/snake deal.
  *
  * Replaces _sorted_desc (balance.py:73-75) + _deal (:59-70) +

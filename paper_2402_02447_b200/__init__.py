@@ -40,6 +40,7 @@ from .strata import (
     draw_batch,
     stratify,
     stratify_lengths,
+    stratify_shards,
 )
 
 __version__ = "0.1.0"
@@ -52,5 +53,5 @@ __all__ = [
     "DEFAULT_BIN_BOUNDARIES", "DEFAULT_BIN_PROBS", "MAX_SEQ_LEN", "LengthDistribution",
     "Sample", "Topology", "generate_corpus", "generate_lengths",
     "DeviceStrata", "Strata", "StratumAllocation", "allocate_counts", "draw_batch",
-    "stratify", "stratify_lengths",
+    "stratify", "stratify_lengths", "stratify_shards",
 ]

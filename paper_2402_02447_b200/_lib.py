@@ -46,6 +46,7 @@ SIGNATURES = {
     ),
     "b2_strata_workspace_bytes": (_SZ, [_I64]),
     "b2_strata_partition": (_I, [_P, _P, _I64, _P, _I, _P, _P, _P, _P, _SZ, _P]),
+    "b2_strata_partition_shards": (_I, [_P, _P, _P, _I, _P, _I, _P, _P, _P, _P, _SZ, _P]),
     "b2_presort_deal": (
         _I,
         [_P, _P, _I64, _I, _I, _I, C.c_int32, C.c_int32, _P, _P, _P, _P, _P],

@@ -104,6 +104,108 @@ __global__ void __launch_bounds__(T) k_presort_deal(const __grid_constant__ Pres
   }
 }
 
+// Warp-per-pool bitonic sort (pools <= 32*K keys, K keys per lane, blocked:
+// element i = lane*K + j).  The composite key is unique per (len, id), so an
+// unstable network yields exactly the reference's stable order whenever the
+// caller does not need input slots (out_pos); ties of identical samples are
+// indistinguishable.  Padding keys (all ones) sort last.
+template <int K>
+__device__ __forceinline__ void warp_bitonic_sort(unsigned long long (&key)[K], int lane) {
+  constexpr int n = 32 * K;
+#pragma unroll
+  for (int size = 2; size <= n; size <<= 1) {
+#pragma unroll
+    for (int d = size >> 1; d > 0; d >>= 1) {
+      if (d >= K) {  // partner in another lane, same slot
+        const int lm = d / K;
+        const bool lower = (lane & lm) == 0;
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          const unsigned long long other = __shfl_xor_sync(0xffffffffu, key[j], lm);
+          const int i = lane * K + j;
+          const bool up = (i & size) == 0;
+          const bool take_min = (lower == up);
+          const unsigned long long mn = key[j] < other ? key[j] : other;
+          const unsigned long long mx = key[j] < other ? other : key[j];
+          key[j] = take_min ? mn : mx;
+        }
+      } else {  // both elements in this lane
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          if ((j & d) == 0) {
+            const int i = lane * K + j;
+            const bool up = (i & size) == 0;
+            const unsigned long long a = key[j], b = key[j | d];
+            if ((a > b) == up) {
+              key[j] = b;
+              key[j | d] = a;
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int K, int WARPS>
+__global__ void __launch_bounds__(32 * WARPS) k_presort_deal_warp(const __grid_constant__ PresortParams p) {
+  constexpr int n = 32 * K;
+  __shared__ int32_t s_ids[WARPS][n];
+  __shared__ int32_t s_lens[WARPS][n];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned long long idmask = (1ull << p.id_bits) - 1ull;
+  const int64_t nwarps = (int64_t)gridDim.x * WARPS;
+  for (int64_t seg = (int64_t)blockIdx.x * WARPS + w; seg < p.nseg; seg += nwarps) {
+    const int64_t base = seg * p.seg_len;
+    unsigned long long key[K];
+    long long first_bad = -1;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const int i = lane * K + j;
+      if (i < p.seg_len) {
+        const int32_t L = p.lens[base + i], D = p.ids[base + i];
+        const bool ok = L >= 1 && L <= p.max_len && D >= 0 && D <= p.max_id;
+        if (!ok && first_bad < 0) first_bad = base + i;
+        key[j] = ((unsigned long long)(uint32_t)(p.max_len - L) << p.id_bits) | (unsigned long long)(uint32_t)D;
+      } else {
+        key[j] = ~0ull;
+      }
+    }
+    if (first_bad >= 0 && p.bad) atomicMin(reinterpret_cast<unsigned long long*>(p.bad), (unsigned long long)first_bad);
+    warp_bitonic_sort<K>(key, lane);
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const int pos = lane * K + j;
+      if (pos < p.seg_len) {
+        const int r = pos / p.lanes, c = pos - r * p.lanes;
+        const int ln = (p.snake && (r & 1)) ? p.lanes - 1 - c : c;  // balance.py:66-67
+        s_ids[w][ln * p.rows + r] = (int32_t)(key[j] & idmask);
+        s_lens[w][ln * p.rows + r] = p.max_len - (int32_t)(key[j] >> p.id_bits);
+      }
+    }
+    __syncwarp();
+    int32_t* out = p.out_ids + base;
+    for (int i = lane; i < p.seg_len; i += 32) out[i] = s_ids[w][i];
+    if (p.tokens)
+      for (int l = lane; l < p.lanes; l += 32) {
+        int64_t sum = 0;  // per-lane token sum (_from_per_gpu, balance.py:54-56)
+        for (int r = 0; r < p.rows; ++r) sum += s_lens[w][l * p.rows + r];
+        p.tokens[seg * p.lanes + l] = sum;
+      }
+    __syncwarp();
+  }
+}
+
+template <int K, int WARPS>
+int launch_warp(const PresortParams& p, cudaStream_t st) {
+  const DeviceInfo& di = device_info();
+  const int64_t blocks = (p.nseg + WARPS - 1) / WARPS;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)di.sm_count * 16));
+  k_presort_deal_warp<K, WARPS><<<grid, 32 * WARPS, 0, st>>>(p);
+  B2_CHECK(cudaGetLastError());
+  return B2_OK;
+}
+
 int bits_for(int64_t v) {  // bits needed to represent 0..v
   int b = 0;
   while (b < 63 && (1ll << b) <= v) ++b;
@@ -156,6 +258,12 @@ extern "C" int b2_presort_deal(const int32_t* ids, const int32_t* lens, int64_t 
   p.tokens = tokens;
   p.bad = bad;
   B2_REQUIRE(p.end_bit <= 64, B2_ERR_UNSUPPORTED, "key does not fit 64 bits");
+  if (!out_pos) {  // no input slots needed: warp-per-pool bitonic network
+    if (seg_len <= 64) return launch_warp<2, 8>(p, st);
+    if (seg_len <= 128) return launch_warp<4, 8>(p, st);
+    if (seg_len <= 256) return launch_warp<8, 4>(p, st);
+    if (seg_len <= 512) return launch_warp<16, 2>(p, st);
+  }
   if (seg_len <= 128) return launch<32, 4>(p, st);
   if (seg_len <= 512) return launch<128, 4>(p, st);
   if (seg_len <= 2048) return launch<256, 8>(p, st);

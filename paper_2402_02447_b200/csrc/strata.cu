@@ -4,16 +4,16 @@
 // searchsorted(bounds, length, side='left') (:74), samples are appended to
 // their stratum in input order (:81), probs = count/N (:82; host side).
 //
-// Three launches, all HBM/L2-streaming (8 B/key algorithmic: 4 B length read,
-// 4 B id written; +4 B if explicit ids are read):
+// Two launches for ALL rank shards at once (HBM/L2-streaming, 8 B/key
+// algorithmic: 4 B length read, 4 B id written; +4 B if explicit ids are read):
 //   k_strata_count  : one CTA per 4096-key tile -> per-tile per-stratum counts
-//                     (+ first bad index via atomicMin)
-//   k_strata_scan   : one CTA, exclusive scan of tile counts per stratum,
-//                     stratum totals
-//   k_strata_scatter: one CTA per tile, stable in-tile ranks from a single
-//                     packed block scan (4 strata x 16-bit fields per u64),
-//                     staged through shared memory so each stratum's run is
-//                     written with consecutive addresses.
+//                     (+ the shard's first bad index via atomicMin)
+//   k_strata_scatter: one CTA per tile sums the counts of the earlier tiles of
+//                     its shard (one L2 round trip instead of a scan launch),
+//                     then places its keys with stable in-tile ranks from a
+//                     single packed block scan (4 strata x 16-bit fields per
+//                     u64), staged through shared memory so each stratum's run
+//                     is written with consecutive addresses.
 #include "common.cuh"
 
 #include <cub/block/block_load.cuh>
@@ -29,17 +29,19 @@ constexpr int kT = 256;            // threads per tile CTA
 constexpr int kItems = 16;         // keys per thread
 constexpr int kTile = kT * kItems; // 4096 keys per tile (fits 16-bit fields)
 
+constexpr int kMaxShards = 64;  // shards (segments) per launch
+
 struct StrataParams {
   const int32_t* len;
-  const int32_t* ids;  // may be null: ids = index
-  int64_t n;
-  int nb;
+  const int32_t* ids;  // may be null: id = index within the shard
+  int nb, nshard;
   int32_t bounds[kMaxStrata];
-  int32_t* tile_counts;  // [T][kMaxStrata]
-  int32_t* tile_off;     // [T][kMaxStrata] exclusive prefix over tiles
-  int64_t* counts;       // [nb] totals
-  int64_t* bad;          // first bad index (u64 min), pre-set to -1
-  int32_t* ids_out;
+  int64_t shard_off[kMaxShards + 1];  // element offset of each shard
+  int32_t tile_off[kMaxShards + 1];   // first tile of each shard
+  int32_t* tile_counts;               // [T][kMaxStrata]
+  int64_t* counts;                    // [nshard][nb] totals
+  int64_t* bad;                       // [nshard] first bad index within the shard (u64 min), pre-set to -1
+  int32_t* ids_out;                   // same offsets as the input
 };
 
 __device__ __forceinline__ int stratum_of(int32_t len, const StrataParams& p) {
@@ -48,6 +50,12 @@ __device__ __forceinline__ int stratum_of(int32_t len, const StrataParams& p) {
   for (int j = 0; j < kMaxStrata; ++j)
     if (j < p.nb) k += (len > p.bounds[j]);  // == searchsorted(..., 'left')
   return k;
+}
+
+__device__ __forceinline__ int shard_of_tile(const StrataParams& p, int tile) {
+  int g = 0;
+  while (g + 1 < p.nshard && p.tile_off[g + 1] <= tile) ++g;
+  return g;
 }
 
 template <int NW>
@@ -66,14 +74,18 @@ struct Packed {
 
 using LoadT = cub::BlockLoad<int32_t, kT, kItems, cub::BLOCK_LOAD_WARP_TRANSPOSE>;
 
+// pass 1: per-tile stratum counts (+ first bad sample of the shard)
 __global__ void __launch_bounds__(kT) k_strata_count(const __grid_constant__ StrataParams p) {
   __shared__ typename LoadT::TempStorage ld;
   __shared__ int cnt[kMaxStrata];
-  const int64_t base = (int64_t)blockIdx.x * kTile;
-  const int valid = (int)min64(kTile, p.n - base);
+  const int tile = blockIdx.x;
+  const int g = shard_of_tile(p, tile);
+  const int64_t sbeg = p.shard_off[g], send = p.shard_off[g + 1];
+  const int64_t lbase = (int64_t)(tile - p.tile_off[g]) * kTile;  // within the shard
+  const int valid = (int)min64(kTile, send - sbeg - lbase);
   if (threadIdx.x < kMaxStrata) cnt[threadIdx.x] = 0;
   int32_t v[kItems];
-  LoadT(ld).Load(p.len + base, v, valid, 1);
+  LoadT(ld).Load(p.len + sbeg + lbase, v, valid, 1);
   __syncthreads();
   int local[kMaxStrata];
 #pragma unroll
@@ -85,12 +97,12 @@ __global__ void __launch_bounds__(kT) k_strata_count(const __grid_constant__ Str
     if (idx < valid) {
       const int k = stratum_of(v[j], p);
       const bool bad = (k == p.nb) || (v[j] < 1);
-      if (bad && first_bad < 0) first_bad = base + idx;
+      if (bad && first_bad < 0) first_bad = lbase + idx;
 #pragma unroll
       for (int q = 0; q < kMaxStrata; ++q) local[q] += (!bad && q == k);
     }
   }
-  if (first_bad >= 0) atomicMin(reinterpret_cast<unsigned long long*>(p.bad), (unsigned long long)first_bad);
+  if (first_bad >= 0) atomicMin(reinterpret_cast<unsigned long long*>(p.bad + g), (unsigned long long)first_bad);
 #pragma unroll
   for (int k = 0; k < kMaxStrata; ++k) {
     if (k < p.nb) {
@@ -101,28 +113,12 @@ __global__ void __launch_bounds__(kT) k_strata_count(const __grid_constant__ Str
     }
   }
   __syncthreads();
-  if (threadIdx.x < p.nb) p.tile_counts[(int64_t)blockIdx.x * kMaxStrata + threadIdx.x] = cnt[threadIdx.x];
+  if (threadIdx.x < p.nb) p.tile_counts[(int64_t)tile * kMaxStrata + threadIdx.x] = cnt[threadIdx.x];
 }
 
-// exclusive scan over tiles, per stratum; one CTA of 1024 threads
-__global__ void __launch_bounds__(1024) k_strata_scan(const __grid_constant__ StrataParams p, int64_t T) {
-  using Scan = cub::BlockScan<int64_t, 1024>;
-  __shared__ typename Scan::TempStorage ts;
-  for (int k = 0; k < p.nb; ++k) {
-    int64_t carry = 0;
-    for (int64_t t0 = 0; t0 < T; t0 += 1024) {
-      const int64_t t = t0 + threadIdx.x;
-      const int64_t c = t < T ? p.tile_counts[t * kMaxStrata + k] : 0;
-      int64_t ex, agg;
-      Scan(ts).ExclusiveSum(c, ex, agg);
-      if (t < T) p.tile_off[t * kMaxStrata + k] = (int32_t)(carry + ex);
-      carry += agg;
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) p.counts[k] = carry;
-  }
-}
-
+// pass 2: each tile sums the counts of the earlier tiles of its shard (one L2
+// round trip, no separate scan launch), then scatters with stable in-tile
+// ranks from a single packed block scan, staged so runs are written coalesced
 template <int NW>
 __global__ void __launch_bounds__(kT) k_strata_scatter(const __grid_constant__ StrataParams p) {
   using Scan = cub::BlockScan<Packed<NW>, kT>;
@@ -134,19 +130,58 @@ __global__ void __launch_bounds__(kT) k_strata_scatter(const __grid_constant__ S
   __shared__ int32_t s_kof[kTile];       // stratum of each staged slot
   __shared__ int64_t s_dst[kMaxStrata];  // global start of this tile's run, per stratum
   __shared__ int32_t s_lstart[kMaxStrata + 1];
-  const int64_t base = (int64_t)blockIdx.x * kTile;
-  const int valid = (int)min64(kTile, p.n - base);
+  __shared__ unsigned long long s_pre[kMaxStrata], s_tot[kMaxStrata];
+  const int tile = blockIdx.x;
+  const int g = shard_of_tile(p, tile);
+  const int64_t sbeg = p.shard_off[g], send = p.shard_off[g + 1];
+  const int64_t lbase = (int64_t)(tile - p.tile_off[g]) * kTile;
+  const int valid = (int)min64(kTile, send - sbeg - lbase);
+  if (threadIdx.x < kMaxStrata) {
+    s_pre[threadIdx.x] = 0ull;
+    s_tot[threadIdx.x] = 0ull;
+  }
+  __syncthreads();
+  {  // prefix over earlier tiles + shard totals, per stratum
+    unsigned long long pre[kMaxStrata], tot[kMaxStrata];
+#pragma unroll
+    for (int k = 0; k < kMaxStrata; ++k) pre[k] = tot[k] = 0ull;
+    for (int t2 = p.tile_off[g] + threadIdx.x; t2 < p.tile_off[g + 1]; t2 += kT) {
+#pragma unroll
+      for (int k = 0; k < kMaxStrata; ++k) {
+        if (k < p.nb) {
+          const unsigned long long cnt = (unsigned long long)p.tile_counts[(int64_t)t2 * kMaxStrata + k];
+          tot[k] += cnt;
+          if (t2 < tile) pre[k] += cnt;
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kMaxStrata; ++k) {
+      if (k < p.nb) {
+        unsigned long long a = pre[k], b = tot[k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          a += __shfl_xor_sync(0xffffffffu, a, o);
+          b += __shfl_xor_sync(0xffffffffu, b, o);
+        }
+        if ((threadIdx.x & 31) == 0) {
+          if (a) atomicAdd(&s_pre[k], a);
+          if (b) atomicAdd(&s_tot[k], b);
+        }
+      }
+    }
+  }
 
   int32_t v[kItems];
-  LoadT(sm.ld).Load(p.len + base, v, valid, 1);
+  LoadT(sm.ld).Load(p.len + sbeg + lbase, v, valid, 1);
   __syncthreads();
   int32_t id[kItems];
   if (p.ids) {
-    LoadT(sm.ld).Load(p.ids + base, id, valid, 0);
+    LoadT(sm.ld).Load(p.ids + sbeg + lbase, id, valid, 0);
     __syncthreads();
   } else {
 #pragma unroll
-    for (int j = 0; j < kItems; ++j) id[j] = (int32_t)(base + threadIdx.x * kItems + j);
+    for (int j = 0; j < kItems; ++j) id[j] = (int32_t)(lbase + threadIdx.x * kItems + j);
   }
   int8_t kk[kItems];
   Packed<NW> mine;
@@ -167,12 +202,13 @@ __global__ void __launch_bounds__(kT) k_strata_scatter(const __grid_constant__ S
   Scan(sm.scan).ExclusiveSum(mine, ex, agg);
   if (threadIdx.x == 0) {
     int acc = 0;
-    int64_t gbase = 0;
+    int64_t gbase = sbeg;
     for (int k = 0; k < p.nb; ++k) {
       s_lstart[k] = acc;
       acc += (int)agg.field(k);
-      s_dst[k] = gbase + p.tile_off[(int64_t)blockIdx.x * kMaxStrata + k];
-      gbase += p.counts[k];
+      s_dst[k] = gbase + (int64_t)s_pre[k];
+      gbase += (int64_t)s_tot[k];
+      if (tile == p.tile_off[g]) p.counts[(int64_t)g * p.nb + k] = (int64_t)s_tot[k];
     }
     s_lstart[p.nb] = acc;
   }
@@ -187,7 +223,10 @@ __global__ void __launch_bounds__(kT) k_strata_scatter(const __grid_constant__ S
       unsigned r = 0;
 #pragma unroll
       for (int q = 0; q < kMaxStrata; ++q)
-        if (q == k) { r = run[q]; run[q] = r + 1; }
+        if (q == k) {
+          r = run[q];
+          run[q] = r + 1;
+        }
       const int slot = s_lstart[k] + (int)ex.field(k) + (int)r;
       sm.stage[slot] = id[j];
       s_kof[slot] = k;
@@ -210,38 +249,45 @@ static inline int64_t strata_tiles(int64_t n) { return (n + kTile - 1) / kTile; 
 
 extern "C" size_t b2_strata_workspace_bytes(int64_t n) {
   if (n < 1) n = 1;
-  return (size_t)strata_tiles(n) * kMaxStrata * sizeof(int32_t) * 2;
+  // per-tile counts; + one partial tile per shard boundary
+  return (size_t)(strata_tiles(n) + kMaxShards) * kMaxStrata * sizeof(int32_t);
 }
 
-extern "C" int b2_strata_partition(const int32_t* lengths, const int32_t* ids, int64_t n,
-                                   const int32_t* bounds, int nb, int32_t* ids_out,
-                                   int64_t* counts, int64_t* bad, void* workspace,
-                                   size_t workspace_bytes, void* stream) {
-  B2_REQUIRE(lengths && ids_out && counts && bad && bounds, B2_ERR_INVALID, "NULL pointer argument");
-  B2_REQUIRE(n >= 1 && n <= INT32_MAX, B2_ERR_INVALID, "n must be in [1, 2^31-1], got %lld", (long long)n);
+extern "C" int b2_strata_partition_shards(const int32_t* lengths, const int32_t* ids, const int64_t* shard_off,
+                                          int nshard, const int32_t* bounds, int nb, int32_t* ids_out,
+                                          int64_t* counts, int64_t* bad, void* workspace, size_t workspace_bytes,
+                                          void* stream) {
+  B2_REQUIRE(lengths && ids_out && counts && bad && bounds && shard_off, B2_ERR_INVALID, "NULL pointer argument");
+  B2_REQUIRE(nshard >= 1 && nshard <= kMaxShards, B2_ERR_UNSUPPORTED, "nshard must be in [1, %d]", kMaxShards);
   B2_REQUIRE(nb >= 1 && nb <= kMaxStrata, B2_ERR_UNSUPPORTED, "nb must be in [1, %d], got %d", kMaxStrata, nb);
   B2_REQUIRE(bounds[0] >= 1, B2_ERR_INVALID, "boundaries must be >= 1");
   for (int k = 1; k < nb; ++k)
     B2_REQUIRE(bounds[k - 1] < bounds[k], B2_ERR_INVALID, "boundaries must be strictly ascending");
-  B2_REQUIRE(workspace && workspace_bytes >= b2_strata_workspace_bytes(n), B2_ERR_INVALID,
-             "strata workspace needs %zu bytes", b2_strata_workspace_bytes(n));
   StrataParams p{};
   p.len = lengths;
   p.ids = ids;
-  p.n = n;
   p.nb = nb;
+  p.nshard = nshard;
   for (int k = 0; k < kMaxStrata; ++k) p.bounds[k] = k < nb ? bounds[k] : INT32_MAX;
-  const int64_t T = strata_tiles(n);
+  int64_t T = 0;
+  p.shard_off[0] = shard_off[0];
+  for (int g = 0; g < nshard; ++g) {
+    const int64_t n = shard_off[g + 1] - shard_off[g];
+    B2_REQUIRE(n >= 1 && n <= INT32_MAX, B2_ERR_INVALID, "shard %d must hold 1..2^31-1 samples", g);
+    p.shard_off[g + 1] = shard_off[g + 1];
+    p.tile_off[g] = (int32_t)T;
+    T += strata_tiles(n);
+  }
+  p.tile_off[nshard] = (int32_t)T;
+  B2_REQUIRE(workspace && workspace_bytes >= (size_t)T * kMaxStrata * sizeof(int32_t), B2_ERR_INVALID,
+             "strata workspace needs %zu bytes", (size_t)T * kMaxStrata * sizeof(int32_t));
   p.tile_counts = static_cast<int32_t*>(workspace);
-  p.tile_off = p.tile_counts + T * kMaxStrata;
   p.counts = counts;
   p.bad = bad;
   p.ids_out = ids_out;
   cudaStream_t st = (cudaStream_t)stream;
-  B2_CHECK(cudaMemsetAsync(bad, 0xff, sizeof(int64_t), st));
+  B2_CHECK(cudaMemsetAsync(bad, 0xff, sizeof(int64_t) * nshard, st));
   k_strata_count<<<(unsigned)T, kT, 0, st>>>(p);
-  B2_CHECK(cudaGetLastError());
-  k_strata_scan<<<1, 1024, 0, st>>>(p, T);
   B2_CHECK(cudaGetLastError());
   const int nw = (nb + 3) / 4;
   if (nw == 1) k_strata_scatter<1><<<(unsigned)T, kT, 0, st>>>(p);
@@ -250,4 +296,13 @@ extern "C" int b2_strata_partition(const int32_t* lengths, const int32_t* ids, i
   else k_strata_scatter<4><<<(unsigned)T, kT, 0, st>>>(p);
   B2_CHECK(cudaGetLastError());
   return B2_OK;
+}
+
+extern "C" int b2_strata_partition(const int32_t* lengths, const int32_t* ids, int64_t n,
+                                   const int32_t* bounds, int nb, int32_t* ids_out, int64_t* counts,
+                                   int64_t* bad, void* workspace, size_t workspace_bytes, void* stream) {
+  B2_REQUIRE(n >= 1 && n <= INT32_MAX, B2_ERR_INVALID, "n must be in [1, 2^31-1], got %lld", (long long)n);
+  const int64_t off[2] = {0, n};
+  return b2_strata_partition_shards(lengths, ids, off, 1, bounds, nb, ids_out, counts, bad, workspace,
+                                    workspace_bytes, stream);
 }

@@ -141,6 +141,46 @@ def stratify_lengths(lengths, boundaries=DEFAULT_STRATUM_BOUNDARIES, ids=None, s
     return DeviceStrata(boundaries=bounds, ids=ids_out, counts=tuple(int(c) for c in counts), probs=probs)
 
 
+def stratify_shards(lengths, shard_offsets: Sequence[int], boundaries=DEFAULT_STRATUM_BOUNDARIES,
+                    stream=None) -> list:
+    """Stratify every rank shard ``lengths[off[g]:off[g+1]]`` in one device pass.
+
+    Equivalent to ``stratify_lengths`` on each shard (ids are shard-local
+    indices); returns one ``DeviceStrata`` per shard (views into one buffer).
+    """
+    bounds = _check_bounds(boundaries)
+    lib = _lib.load()
+    lens = _as_i32_device(lengths, "lengths")
+    offs = [int(o) for o in shard_offsets]
+    if len(offs) < 2 or offs[0] != 0 or offs[-1] != lens.numel() or any(a >= b for a, b in zip(offs, offs[1:])):
+        raise ValueError("shard_offsets must start at 0, end at len(lengths) and be strictly increasing")
+    ns = len(offs) - 1
+    dev = lens.device
+    ws_bytes = lib.b2_strata_workspace_bytes(lens.numel())
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    ids_out = torch.empty(lens.numel(), dtype=torch.int32, device=dev)
+    counts = torch.empty((ns, len(bounds)), dtype=torch.int64, device=dev)
+    bad = torch.empty(ns, dtype=torch.int64, device=dev)
+    rc = lib.b2_strata_partition_shards(
+        lens.data_ptr(), None, _lib.i64_array(offs), ns, _lib.i32_array(bounds), len(bounds), ids_out.data_ptr(),
+        counts.data_ptr(), bad.data_ptr(), ws.data_ptr(), ws_bytes, _lib.stream_ptr(stream))
+    _lib.check(rc)
+    host = torch.cat([bad, counts.reshape(-1)]).cpu().tolist()
+    out = []
+    for g in range(ns):
+        if host[g] >= 0:
+            i = host[g]
+            length = int(lens[offs[g] + i])
+            if length < 1:
+                raise ValueError(f"sample length must be >= 1, got {length}")
+            raise ValueError(f"sample id {i} has length {length}, beyond the last stratum boundary {bounds[-1]}")
+        cnt = tuple(int(c) for c in host[ns + g * len(bounds): ns + (g + 1) * len(bounds)])
+        n = offs[g + 1] - offs[g]
+        out.append(DeviceStrata(boundaries=bounds, ids=ids_out[offs[g]:offs[g + 1]], counts=cnt,
+                                probs=tuple(c / n for c in cnt)))
+    return out
+
+
 def stratify(samples: Sequence[Sample], boundaries=DEFAULT_STRATUM_BOUNDARIES) -> Strata:
     """Partition samples into strata by length, preserving input order (strata.py:61-83)."""
     bounds = _check_bounds(boundaries)

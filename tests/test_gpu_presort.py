@@ -26,6 +26,7 @@ from paper_2402_02447_b200 import (  # noqa: E402
     presort_deal,
     stratify,
     stratify_lengths,
+    stratify_shards,
 )
 from paper_2402_02447_b200 import synthetic  # noqa: E402
 
@@ -93,13 +94,32 @@ def test_stratify_full_config():
     """10M Wikipedia-like lengths, 8 rank shards of 1.25M: bit-exact per shard."""
     lens = synthetic_lengths()
     shard = lens.size // 8
+    offs = [r * shard for r in range(9)]
+    sharded = stratify_shards(lens, offs, BOUNDS)  # one device pass over all shards
     for r in range(8):
         part = lens[r * shard:(r + 1) * shard]
         ids = np.arange(r * shard, (r + 1) * shard, dtype=np.int32)
         ds = stratify_lengths(part, BOUNDS, ids=ids)
         pools, probs = O.stratify(part, BOUNDS, ids=ids)
-        assert ds.probs == probs
+        assert ds.probs == probs and sharded[r].probs == probs
         np.testing.assert_array_equal(ds.ids.cpu().numpy(), np.concatenate(pools))
+        np.testing.assert_array_equal(sharded[r].ids.cpu().numpy() + r * shard, np.concatenate(pools))
+
+
+def test_stratify_shards_ragged_and_errors():
+    rng = np.random.default_rng(9)
+    sizes = [1, 4095, 4096, 4097, 10_000, 3]
+    offs = np.concatenate([[0], np.cumsum(sizes)]).tolist()
+    lens = rng.integers(1, 513, size=offs[-1]).astype(np.int32)
+    out = stratify_shards(lens, offs, BOUNDS)
+    for g in range(len(sizes)):
+        part = lens[offs[g]:offs[g + 1]]
+        pools, probs = O.stratify(part, BOUNDS)
+        assert out[g].probs == probs
+        np.testing.assert_array_equal(out[g].ids.cpu().numpy(), np.concatenate(pools))
+    lens[offs[4] + 77] = 999
+    with pytest.raises(ValueError, match="id 77 has length 999"):
+        stratify_shards(lens, offs, BOUNDS)
 
 
 _LENS = None
