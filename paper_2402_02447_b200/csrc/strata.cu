@@ -44,11 +44,11 @@ struct StrataParams {
   int32_t* ids_out;                   // same offsets as the input
 };
 
+template <int NB>
 __device__ __forceinline__ int stratum_of(int32_t len, const StrataParams& p) {
   int k = 0;
 #pragma unroll
-  for (int j = 0; j < kMaxStrata; ++j)
-    if (j < p.nb) k += (len > p.bounds[j]);  // == searchsorted(..., 'left')
+  for (int j = 0; j < NB; ++j) k += (len > p.bounds[j]);  // == searchsorted(..., 'left'); unused bounds are INT32_MAX
   return k;
 }
 
@@ -75,6 +75,7 @@ struct Packed {
 using LoadT = cub::BlockLoad<int32_t, kT, kItems, cub::BLOCK_LOAD_WARP_TRANSPOSE>;
 
 // pass 1: per-tile stratum counts (+ first bad sample of the shard)
+template <int NB>
 __global__ void __launch_bounds__(kT) k_strata_count(const __grid_constant__ StrataParams p) {
   __shared__ typename LoadT::TempStorage ld;
   __shared__ int cnt[kMaxStrata];
@@ -87,40 +88,49 @@ __global__ void __launch_bounds__(kT) k_strata_count(const __grid_constant__ Str
   int32_t v[kItems];
   LoadT(ld).Load(p.len + sbeg + lbase, v, valid, 1);
   __syncthreads();
-  int local[kMaxStrata];
+  // per-thread counts packed 16 bits per stratum (<= kItems each), 4 strata per u64
+  constexpr int NW = (NB + 3) / 4;
+  unsigned long long local[NW];
 #pragma unroll
-  for (int k = 0; k < kMaxStrata; ++k) local[k] = 0;
+  for (int i = 0; i < NW; ++i) local[i] = 0ull;
   long long first_bad = -1;
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
     const int idx = threadIdx.x * kItems + j;
     if (idx < valid) {
-      const int k = stratum_of(v[j], p);
-      const bool bad = (k == p.nb) || (v[j] < 1);
+      const int k = stratum_of<NB>(v[j], p);
+      const bool bad = (k >= p.nb) || (v[j] < 1);
       if (bad && first_bad < 0) first_bad = lbase + idx;
+      if (!bad) {
 #pragma unroll
-      for (int q = 0; q < kMaxStrata; ++q) local[q] += (!bad && q == k);
+        for (int i = 0; i < NW; ++i)
+          if ((k >> 2) == i) local[i] += 1ull << ((k & 3) * 16);
+      }
     }
   }
   if (first_bad >= 0) atomicMin(reinterpret_cast<unsigned long long*>(p.bad + g), (unsigned long long)first_bad);
 #pragma unroll
-  for (int k = 0; k < kMaxStrata; ++k) {
-    if (k < p.nb) {
-      int s = local[k];
+  for (int i = 0; i < NW; ++i) {  // warp sums stay < 2^16 per field (32 x 16 keys)
+    unsigned long long s2 = local[i];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if ((threadIdx.x & 31) == 0 && s) atomicAdd(&cnt[k], s);
-    }
+    for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    if ((threadIdx.x & 31) == 0)
+#pragma unroll
+      for (int f = 0; f < 4; ++f) {
+        const unsigned c = (unsigned)((s2 >> (16 * f)) & 0xffffull);
+        if (c && 4 * i + f < NB) atomicAdd(&cnt[4 * i + f], (int)c);
+      }
   }
   __syncthreads();
-  if (threadIdx.x < p.nb) p.tile_counts[(int64_t)tile * kMaxStrata + threadIdx.x] = cnt[threadIdx.x];
+  if (threadIdx.x < NB) p.tile_counts[(int64_t)tile * kMaxStrata + threadIdx.x] = threadIdx.x < p.nb ? cnt[threadIdx.x] : 0;
 }
 
 // pass 2: each tile sums the counts of the earlier tiles of its shard (one L2
 // round trip, no separate scan launch), then scatters with stable in-tile
 // ranks from a single packed block scan, staged so runs are written coalesced
-template <int NW>
+template <int NB>
 __global__ void __launch_bounds__(kT) k_strata_scatter(const __grid_constant__ StrataParams p) {
+  constexpr int NW = (NB + 3) / 4;
   using Scan = cub::BlockScan<Packed<NW>, kT>;
   __shared__ union {
     typename LoadT::TempStorage ld;
@@ -142,22 +152,20 @@ __global__ void __launch_bounds__(kT) k_strata_scatter(const __grid_constant__ S
   }
   __syncthreads();
   {  // prefix over earlier tiles + shard totals, per stratum
-    unsigned long long pre[kMaxStrata], tot[kMaxStrata];
+    unsigned long long pre[NB], tot[NB];
 #pragma unroll
-    for (int k = 0; k < kMaxStrata; ++k) pre[k] = tot[k] = 0ull;
+    for (int k = 0; k < NB; ++k) pre[k] = tot[k] = 0ull;
     for (int t2 = p.tile_off[g] + threadIdx.x; t2 < p.tile_off[g + 1]; t2 += kT) {
 #pragma unroll
-      for (int k = 0; k < kMaxStrata; ++k) {
-        if (k < p.nb) {
-          const unsigned long long cnt = (unsigned long long)p.tile_counts[(int64_t)t2 * kMaxStrata + k];
-          tot[k] += cnt;
-          if (t2 < tile) pre[k] += cnt;
-        }
+      for (int k = 0; k < NB; ++k) {
+        const unsigned long long cnt = (unsigned long long)p.tile_counts[(int64_t)t2 * kMaxStrata + k];
+        tot[k] += cnt;
+        if (t2 < tile) pre[k] += cnt;
       }
     }
 #pragma unroll
-    for (int k = 0; k < kMaxStrata; ++k) {
-      if (k < p.nb) {
+    for (int k = 0; k < NB; ++k) {
+      {
         unsigned long long a = pre[k], b = tot[k];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -192,8 +200,8 @@ __global__ void __launch_bounds__(kT) k_strata_scatter(const __grid_constant__ S
     const int idx = threadIdx.x * kItems + j;
     int k = -1;
     if (idx < valid) {
-      k = stratum_of(v[j], p);
-      if (k == p.nb || v[j] < 1) k = -1;  // bad samples are reported, not placed
+      k = stratum_of<NB>(v[j], p);
+      if (k >= p.nb || v[j] < 1) k = -1;  // bad samples are reported, not placed
     }
     kk[j] = (int8_t)k;
     if (k >= 0) mine.w[k >> 2] += 1ull << ((k & 3) * 16);
@@ -213,16 +221,16 @@ __global__ void __launch_bounds__(kT) k_strata_scatter(const __grid_constant__ S
     s_lstart[p.nb] = acc;
   }
   __syncthreads();  // also retires the scan temp storage before staging
-  unsigned run[kMaxStrata];
+  unsigned run[NB];
 #pragma unroll
-  for (int k = 0; k < kMaxStrata; ++k) run[k] = 0;
+  for (int k = 0; k < NB; ++k) run[k] = 0;
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
     const int k = kk[j];
     if (k >= 0) {
       unsigned r = 0;
 #pragma unroll
-      for (int q = 0; q < kMaxStrata; ++q)
+      for (int q = 0; q < NB; ++q)
         if (q == k) {
           r = run[q];
           run[q] = r + 1;
@@ -287,13 +295,19 @@ extern "C" int b2_strata_partition_shards(const int32_t* lengths, const int32_t*
   p.ids_out = ids_out;
   cudaStream_t st = (cudaStream_t)stream;
   B2_CHECK(cudaMemsetAsync(bad, 0xff, sizeof(int64_t) * nshard, st));
-  k_strata_count<<<(unsigned)T, kT, 0, st>>>(p);
-  B2_CHECK(cudaGetLastError());
-  const int nw = (nb + 3) / 4;
-  if (nw == 1) k_strata_scatter<1><<<(unsigned)T, kT, 0, st>>>(p);
-  else if (nw == 2) k_strata_scatter<2><<<(unsigned)T, kT, 0, st>>>(p);
-  else if (nw == 3) k_strata_scatter<3><<<(unsigned)T, kT, 0, st>>>(p);
-  else k_strata_scatter<4><<<(unsigned)T, kT, 0, st>>>(p);
+  if (nb <= 4) {
+    k_strata_count<4><<<(unsigned)T, kT, 0, st>>>(p);
+    B2_CHECK(cudaGetLastError());
+    k_strata_scatter<4><<<(unsigned)T, kT, 0, st>>>(p);
+  } else if (nb <= 8) {
+    k_strata_count<8><<<(unsigned)T, kT, 0, st>>>(p);
+    B2_CHECK(cudaGetLastError());
+    k_strata_scatter<8><<<(unsigned)T, kT, 0, st>>>(p);
+  } else {
+    k_strata_count<16><<<(unsigned)T, kT, 0, st>>>(p);
+    B2_CHECK(cudaGetLastError());
+    k_strata_scatter<16><<<(unsigned)T, kT, 0, st>>>(p);
+  }
   B2_CHECK(cudaGetLastError());
   return B2_OK;
 }

@@ -102,3 +102,53 @@ def test_ddp_comm_hook_two_ranks_single_bucket():
     for r in range(WORLD):
         np.testing.assert_allclose(res[r][1], ref, rtol=0, atol=1e-6 * np.abs(ref).max())
     assert np.linalg.norm(ref) <= 0.5 + 1e-9
+
+
+LB = 16
+STEPS = 5
+
+
+def _draws(rank):
+    rng = np.random.default_rng(50 + rank)
+    ids = rng.permutation(100_000)[: STEPS * LB].reshape(STEPS, LB).astype(np.int32) + 100_000 * rank
+    lens = rng.integers(1, 513, size=(STEPS, LB)).astype(np.int32)
+    return ids, lens
+
+
+def _oracle_deal(ids, lens, seg_len, lanes, scan):
+    from oracle import ddp_oracle as O
+
+    out, tok = O.presort_deal_segments(ids.numpy(), lens.numpy(), seg_len, lanes, scan.value == "snake")
+    return torch.from_numpy(out), torch.from_numpy(tok)
+
+
+def _presort_worker(rank, port, q):
+    import torch.distributed as dist
+
+    from paper_2402_02447_b200 import Topology
+    from paper_2402_02447_b200.presort_dist import LocalPresort
+
+    H.init(rank, WORLD, port, "gloo")
+    try:
+        ids, lens = _draws(rank)
+        lp = LocalPresort(Topology(1, WORLD), LB, 512, 10**6, "snake", deal=_oracle_deal)
+        steps = [lp.step(torch.from_numpy(ids[t]), torch.from_numpy(lens[t])) for t in range(STEPS)]
+        ep_ids, ep_tok = lp.epoch(torch.from_numpy(ids), torch.from_numpy(lens))
+        q.put((rank, ([o.numpy() for o, _ in steps], [t.numpy() for _, t in steps]), (ep_ids.numpy(), ep_tok.numpy())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_local_presort_two_ranks_matches_reference_semantics():
+    from oracle import ddp_oracle as O
+
+    res = _run(_presort_worker)
+    draws = [_draws(r) for r in range(WORLD)]
+    for t in range(STEPS):
+        per_gpu, tok = O.assign_local_presort([d[0][t] for d in draws], [d[1][t] for d in draws], 1, WORLD, True)
+        for r in range(WORLD):
+            (step_ids, step_tok), (ep_ids, ep_tok) = res[r]
+            assert step_ids[t].tolist() == per_gpu[r]
+            assert step_tok[t].tolist() == list(tok)
+            assert ep_ids[t].tolist() == per_gpu[r]
+            assert ep_tok[t].tolist() == list(tok)

@@ -161,3 +161,40 @@ def test_fused_clip_allreduce_p2p_matches_reference():
             np.testing.assert_array_equal(out, first)
         rn = np.array([np.linalg.norm(W[r, a:b]) for a, b in LAYOUT8])
         np.testing.assert_allclose(res[r]["norms"], rn, rtol=1e-6)
+
+
+def _presort_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    from paper_2402_02447_b200 import Topology
+    from paper_2402_02447_b200.presort_dist import LocalPresort
+
+    H.init(rank, world, port, "nccl")
+    try:
+        rng = np.random.default_rng(70 + rank)
+        ids = (rng.permutation(1_000_000)[: 200 * 48].reshape(200, 48) + 1_000_000 * rank).astype(np.int32)
+        lens = rng.integers(1, 513, size=(200, 48)).astype(np.int32)
+        lp = LocalPresort(Topology(1, world), 48, 512, 10_000_000, "snake")
+        step_ids, step_tok = lp.step(torch.from_numpy(ids[0]).cuda(), torch.from_numpy(lens[0]).cuda())
+        ep_ids, ep_tok = lp.epoch(torch.from_numpy(ids).cuda(), torch.from_numpy(lens).cuda())
+        q.put((rank, {"ids": ids, "lens": lens, "step": step_ids.cpu().numpy(), "step_tok": step_tok.cpu().numpy(),
+                      "ep": ep_ids.cpu().numpy(), "ep_tok": ep_tok.cpu().numpy()}))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_local_presort_nccl_matches_reference():
+    from oracle import ddp_oracle as O
+
+    world = _world()
+    res = _run(_presort_worker, world)
+    for t in range(200):
+        per_gpu, tok = O.assign_local_presort([res[r]["ids"][t] for r in range(world)],
+                                              [res[r]["lens"][t] for r in range(world)], 1, world, True)
+        for r in range(world):
+            assert res[r]["ep"][t].tolist() == per_gpu[r]
+            assert res[r]["ep_tok"][t].tolist() == list(tok)
+            if t == 0:
+                assert res[r]["step"].tolist() == per_gpu[r]
+                assert res[r]["step_tok"].tolist() == list(tok)

@@ -40,11 +40,14 @@ def main():
             clip.clip_cast(g, comm, segs, lim)
         torch.cuda.synchronize()
         del g, comm
-    if a.only in ("all", "strata", "presort"):
+    if a.only in ("all", "strata", "strata_shards", "presort"):
         lens = B.seqdata.generate_lengths(B.LengthDistribution(), 10_000_000, 2402)
         if a.only in ("all", "strata"):
             for r in range(2):
                 B.stratify_lengths(lens[r * 1_250_000:(r + 1) * 1_250_000])
+        if a.only in ("all", "strata_shards"):
+            for _ in range(a.iters):
+                B.stratify_shards(lens, [r * 1_250_000 for r in range(9)])
         if a.only in ("all", "presort"):
             n = 26_000 * 384
             ids = np.arange(n, dtype=np.int32)
