@@ -552,6 +552,7 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-presort", action="store_true")
+    ap.add_argument("--no-bert", action="store_true")
     ap.add_argument("--comm", choices=("fused", "nccl"), default="fused",
                     help="N>1: fused clip+NVLink allreduce kernel (default) or per-bucket NCCL")
     args = ap.parse_args()
@@ -567,6 +568,20 @@ def main():
     rank, world, local = dist_init(args.gpus)
     r = bench_clip(args, rank, world, local)
     sample = r.pop("_cpu_sample")
+    bert = None
+    if not args.no_bert:  # BERT-large MLPerf phase-2 step under the three clip disciplines (all ranks)
+        try:
+            from paper_2402_02447_b200.train_step import bert_large_step_bench
+
+            bert = {}
+            for mode in ("stock", "after", "bucketwise"):
+                r_ = bert_large_step_bench(mode, steps=max(3, min(args.steps, 10)), warmup=2)
+                bert[mode] = {"samples_per_s": r_["samples_per_s"], "ms_per_step": r_["ms_per_step"]}
+                if "buckets" in r_:
+                    bert[mode]["buckets"] = r_["buckets"]
+            bert["config"] = "BertForPreTraining 336M (random init), seq 512, batch 48/GPU, bf16 autocast, AdamW, DDP 25 MiB buckets"
+        except Exception as e:  # transformers missing etc.: report, do not fail the bench
+            bert = {"error": str(e)[:200]}
     presort = None
     if rank == 0 and not args.no_presort:
         presort = bench_presort(args)
@@ -585,6 +600,8 @@ def main():
         }
         if "nvlink" in r:
             line["nvlink"] = r["nvlink"]
+        if bert is not None:
+            line["bert_large_train"] = bert
         if presort is not None:
             line["presort"] = {"metric": "presort keys/s", "unit": "keys/s",
                                "config": "10M lengths (seed 2402) over 8 shards, Topology(1,8), snake, whole epoch",
