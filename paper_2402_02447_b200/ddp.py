@@ -227,8 +227,6 @@ class FusedBucketSync:
             raise ValueError(f"config mode is {cfg.mode.value}, expected {ClipMode.BUCKET_WISE.value}")
         self.lib = _lib.load()
         self.layout = tuple((int(a), int(b)) for a, b in layout)
-        if len(self.layout) > 128:
-            raise ValueError("fused sync supports at most 128 buckets per step")
         if any(a % 8 or (b - a) % 8 for a, b in self.layout):
             raise ValueError("fused sync needs 8-element aligned buckets")
         self.limit = cfg.threshold / math.sqrt(len(self.layout))  # gradsync.py:155
@@ -265,8 +263,13 @@ class FusedBucketSync:
         self._flags = (ctypes.c_void_p * self.world)(*flags)
         self.clipper = BucketClipper(device=self.device)
         order = list(reversed(range(len(self.layout))))  # backward order (:157)
-        self._offs = _lib.i64_array(self.layout[b][0] for b in order)
-        self._lens = _lib.i64_array(self.layout[b][1] - self.layout[b][0] for b in order)
+        # one launch per <= 128 buckets (the kernel's segment table); each launch is a full
+        # clip + allreduce of its buckets with its own epoch
+        self._chunks = []
+        for c0 in range(0, len(order), 128):
+            part = order[c0:c0 + 128]
+            self._chunks.append((c0, len(part), _lib.i64_array(self.layout[b][0] for b in part),
+                                 _lib.i64_array(self.layout[b][1] - self.layout[b][0] for b in part)))
         self._norms_call = torch.zeros(len(self.layout), dtype=torch.float64, device=self.device)
         torch.cuda.synchronize(self.device)
         dist.barrier(group=group)
@@ -275,10 +278,11 @@ class FusedBucketSync:
         if grad.numel() != self.dim or grad.dtype != torch.float32 or not grad.is_cuda:
             raise ValueError(f"expected a CUDA float32 gradient of {self.dim} elements")
         ws = self.clipper.workspace
-        _lib.check(self.lib.b2_bucket_clip_allreduce_p2p(
-            grad.data_ptr(), self._stages, self._flags, self.world, self.rank, self._offs, self._lens,
-            len(self.layout), float(self.limit), self._norms_call.data_ptr(), None, ws.data_ptr(), ws.numel(),
-            _lib.stream_ptr(stream)))
+        sp = _lib.stream_ptr(stream)
+        for c0, n, offs, lens in self._chunks:
+            _lib.check(self.lib.b2_bucket_clip_allreduce_p2p(
+                grad.data_ptr(), self._stages, self._flags, self.world, self.rank, offs, lens, n,
+                float(self.limit), self._norms_call[c0:].data_ptr(), None, ws.data_ptr(), ws.numel(), sp))
         return self.stage
 
     @property

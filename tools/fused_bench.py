@@ -25,6 +25,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--mb", type=int, default=25, help="bucket size in MiB of fp32")
+    ap.add_argument("--comm", choices=("fused", "nccl"), default="fused")
     args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -37,15 +38,25 @@ def main():
     dim = synthetic.BERT_LARGE_DIM
     g, _, _ = synthetic.bert_grads(dim, rank=rank)
     layout = B.capped_bucket_layout(dim, args.mb * 1024 * 1024 // 4)
-    sync = FusedBucketSync(layout, B.ClipConfig(1.0, "bucket_wise"))
+    if args.comm == "fused":
+        sync = FusedBucketSync(layout, B.ClipConfig(1.0, "bucket_wise"))
+        fn = lambda s_: sync.sync(g, stream=s_)  # noqa: E731
+    else:
+        from paper_2402_02447_b200.ddp import BucketwiseSync
+
+        sync = BucketwiseSync(layout, B.ClipConfig(1.0, "bucket_wise"), comm_dtype=torch.bfloat16)
+
+        def fn(s_):
+            sync.sync_native(g, stream=s_)
+            s_.wait_stream(sync.side)
     cap = torch.cuda.Stream()
     cap.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(cap):
-        sync.sync(g, stream=cap)
+        fn(cap)
     torch.cuda.synchronize()
     graph = torch.cuda.CUDAGraph()
     with torch.cuda.graph(graph, stream=cap):
-        sync.sync(g, stream=cap)
+        fn(cap)
     for _ in range(3):
         graph.replay()
     torch.cuda.synchronize()
@@ -61,10 +72,11 @@ def main():
     ms = float(t.item())
     algbw = dim * 2 / (ms * 1e-3) / 1e9
     if rank == 0:
-        print(json.dumps({"world": world, "cfg": os.environ.get("B2_FUSED_CFG", "0"), "bucket_mb": args.mb,
+        print(json.dumps({"world": world, "comm": args.comm, "cfg": os.environ.get("B2_FUSED_CFG", "0"), "bucket_mb": args.mb,
                           "buckets": len(layout), "ms": ms, "busbw_gbs": algbw * 2 * (world - 1) / world,
                           "grad_gbs_per_rank": dim * 4 / (ms * 1e-3) / 1e9}), flush=True)
-    sync.close()
+    if hasattr(sync, "close"):
+        sync.close()
     dist.destroy_process_group()
 
 
