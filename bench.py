@@ -376,28 +376,73 @@ def bench_clip(args, rank, world, local):
 
 # --------------------------------------------------------------------- H2 (ours)
 def presort_inputs():
-    from oracle import ddp_oracle as O  # input prep only (allocation uses host probs)
-    from paper_2402_02447_b200 import synthetic
+    """10M-sample corpus, 8 rank shards; per rank, an epoch of REAL reference draws.
+
+    Strata per shard come from K2 (stratify_shards); every rank's draws are
+    draw_batch with seed derive_seed(2402, rank, step) (seeding.py:18-21),
+    produced by the bit-exact native port (NativeDraws) on host threads.
+    Returns (lengths, {lb: (pool_ids, pool_lens, steps)}, draw_stats).
+    """
+    from concurrent.futures import ThreadPoolExecutor
+
+    import paper_2402_02447_b200 as B
     from paper_2402_02447_b200.seqdata import LengthDistribution, generate_lengths
 
     lens = generate_lengths(LengthDistribution(), CORPUS_N, CORPUS_SEED)
     shard = CORPUS_N // SHARDS
-    out = {}
+    strata = B.stratify_shards(lens, [r * shard for r in range(SHARDS + 1)], BOUNDS)
+    shard_pools = []
+    for r, ds in enumerate(strata):
+        ids = ds.ids.cpu().numpy().astype(np.int64) + r * shard
+        o = np.concatenate([[0], np.cumsum(ds.counts)])
+        shard_pools.append(([ids[o[k]:o[k + 1]] for k in range(len(BOUNDS))], ds.probs))
+    out, stats = {}, {}
     for lb in (16, 48):
-        ids_r, lens_r = [], []
+        def rank_epoch(r):
+            pools, probs = shard_pools[r]
+            counts = B.allocate_counts(probs, lb).counts
+            nd = B.NativeDraws(pools, BOUNDS)
+            ids, done = nd.epoch(counts, CORPUS_SEED, key=(r,), nsteps=shard // lb + 1)
+            nd.close()
+            return ids.astype(np.int32), done
+
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(max_workers=SHARDS) as ex:
+            res = list(ex.map(rank_epoch, range(SHARDS)))
+        dt = time.perf_counter() - t0
+        steps = min(d for _, d in res)
+        ids = np.stack([x[:steps] for x, _ in res], axis=1).reshape(-1)  # pool of step t: GPU 0..7 draws
+        out[lb] = (ids, lens[ids].astype(np.int32), steps)
+        stats[lb] = {"keys": int(sum(d for _, d in res) * lb), "seconds": dt,
+                     "keys_per_s": sum(d for _, d in res) * lb / dt, "threads": SHARDS,
+                     "impl": "NativeDraws (bit-exact numpy PCG64 draw_batch port, host C++)"}
+    return lens, out, stats
+
+
+def reference_presort_inputs():
+    """Reference arm (CPU only): same corpus, pools of the first 20k node-steps from oracle draws."""
+    from oracle import ddp_oracle as O
+
+    lens = O.generate_lengths(CORPUS_N, CORPUS_SEED)
+    shard = CORPUS_N // SHARDS
+    out = {}
+    for lb in (48,):
+        ids_r = []
         for r in range(SHARDS):
             part = lens[r * shard:(r + 1) * shard]
-            k = np.searchsorted(np.asarray(BOUNDS), part, side="left")
-            probs = tuple(int(c) / part.size for c in np.bincount(k, minlength=4))
+            pools, probs = O.stratify(part)
+            pl = [(p + r * shard).tolist() for p in pools]
             counts = O.allocate_counts(probs, lb)
-            i, l = synthetic.epoch_draws(part, BOUNDS, counts, None, seed=100 + r)
-            ids_r.append(i + r * shard)
-            lens_r.append(l)
-        steps = min(x.shape[0] for x in ids_r)
-        ids = np.stack([x[:steps] for x in ids_r], axis=1).reshape(-1)
-        ln = np.stack([x[:steps] for x in lens_r], axis=1).reshape(-1)
-        out[lb] = (ids, ln, steps)
+            steps = 200  # bounded sample: the oracle's Python draw loop is slow
+            ids_r.append(np.array([O.draw_batch(pl, BOUNDS, counts, O_derive(r, t)) for t in range(steps)]))
+        ids = np.stack(ids_r, axis=1).reshape(-1).astype(np.int32)
+        out[lb] = (ids, lens[ids].astype(np.int32), 200)
     return lens, out
+
+
+def O_derive(r, t):
+    s = np.random.SeedSequence(entropy=CORPUS_SEED, spawn_key=(r, t))
+    return int(s.generate_state(1, np.uint64)[0])
 
 
 def bench_presort(args):
@@ -406,7 +451,7 @@ def bench_presort(args):
     import paper_2402_02447_b200 as B
     from paper_2402_02447_b200 import _lib
 
-    lens, pools = presort_inputs()
+    lens, pools, draw_stats = presort_inputs()
     lib = _lib.load()
     shard = CORPUS_N // SHARDS
     d_lens = torch.from_numpy(lens).cuda()
@@ -425,7 +470,7 @@ def bench_presort(args):
             d_lens.data_ptr(), None, offs, SHARDS, bnds, 4, ids_out.data_ptr(), counts.data_ptr(),
             bad.data_ptr(), ws.data_ptr(), ws_bytes, sp))
 
-    res = {}
+    res = {"draws": {f"lb{k}": v for k, v in draw_stats.items()}}
     for lb in (16, 48):
         ids, ln, steps = pools[lb]
         d_ids, d_ln = torch.from_numpy(ids).cuda(), torch.from_numpy(ln).cuda()
@@ -536,7 +581,7 @@ def run_reference(args, rank, world):
         O.sync_bucketwise(w, layout, lim)
     s = (time.perf_counter() - t) / args.steps
     v = w.size * 4 / s / 1e9
-    lens, pools = presort_inputs()
+    lens, pools = reference_presort_inputs()
     pre = cpu_presort_baseline(lens, pools)
     return {
         "metric": "clip+allreduce GB/s", "value": v, "unit": "GB/s", "impl": "reference",
@@ -619,7 +664,7 @@ def main():
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_clip_baseline(sample, 52)
             if presort is not None:
-                lens, pools = presort_inputs()
+                lens, pools, _ = presort_inputs()
                 line["presort"]["cpu_baseline"] = cpu_presort_baseline(lens, pools)
         print(json.dumps(line), flush=True)
     if world > 1:

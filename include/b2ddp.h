@@ -169,6 +169,27 @@ int b2_strata_partition_shards(const int32_t* lengths, const int32_t* ids, const
                                const int32_t* bounds, int nb, int32_t* ids_out, int64_t* counts, int64_t* bad,
                                void* workspace, size_t workspace_bytes, void* stream);
 
+/* Draws (host, CPU) — bit-exact native port of the reference's stratified
+ * draws: numpy's SeedSequence -> PCG64 -> Generator.choice(replace=False)
+ * (tail shuffle / Floyd), descending swap-pop and closest-boundary borrowing
+ * of draw_batch (strata.py:113-161), and derive_seed (seeding.py:18-21).
+ * A b2_draw_state owns mutable per-stratum id pools (the Strata buckets);
+ * draws consume them like the reference.  Global exhaustion returns
+ * B2_ERR_INVALID with the reference's stratum number / shortfall. */
+typedef struct b2_draw_state b2_draw_state;
+uint64_t b2_derive_seed(uint64_t seed, const uint64_t* key, int nkey);
+int b2_draws_create(b2_draw_state** st, const int64_t* pool_ids, const int64_t* pool_sizes, int nstrata,
+                    const int64_t* bounds);
+int b2_draws_destroy(b2_draw_state* st);
+int64_t b2_draws_remaining(const b2_draw_state* st, int stratum);
+int b2_draw_batch(b2_draw_state* st, const int64_t* counts, uint64_t seed, int64_t* out, int* err_stratum,
+                  int64_t* err_short);
+/* steps t = 0..nsteps-1 with seed derive_seed(base_seed, key..., first_step + t)
+ * (nkey <= 7); out is [nsteps][sum(counts)]; *done = completed steps. */
+int b2_draw_epoch(b2_draw_state* st, const int64_t* counts, uint64_t base_seed, const uint64_t* key, int nkey,
+                  int64_t first_step, int64_t nsteps, int64_t* out, int64_t* done, int* err_stratum,
+                  int64_t* err_short);
+
 /* K3 — per-pool stable sort by (-length, id) + raster/snake deal.
  *
  * Replaces _sorted_desc (balance.py:73-75) + _deal (:59-70) +

@@ -41,6 +41,8 @@ from .strata import (
     stratify,
     stratify_lengths,
     stratify_shards,
+    NativeDraws,
+    derive_seed,
 )
 
 __version__ = "0.1.0"
@@ -53,5 +55,5 @@ __all__ = [
     "DEFAULT_BIN_BOUNDARIES", "DEFAULT_BIN_PROBS", "MAX_SEQ_LEN", "LengthDistribution",
     "Sample", "Topology", "generate_corpus", "generate_lengths",
     "DeviceStrata", "Strata", "StratumAllocation", "allocate_counts", "draw_batch",
-    "stratify", "stratify_lengths", "stratify_shards",
+    "stratify", "stratify_lengths", "stratify_shards", "NativeDraws", "derive_seed",
 ]

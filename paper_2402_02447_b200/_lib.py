@@ -44,6 +44,16 @@ SIGNATURES = {
         _I,
         [_P, _P, _P, _I, _I, _P, _P, _I, _D, _P, _P, _P, _SZ, _P],
     ),
+    "b2_derive_seed": (C.c_uint64, [C.c_uint64, _P, _I]),
+    "b2_draws_create": (_I, [C.POINTER(C.c_void_p), _P, _P, _I, _P]),
+    "b2_draws_destroy": (_I, [_P]),
+    "b2_draws_remaining": (_I64, [_P, _I]),
+    "b2_draw_batch": (_I, [_P, _P, C.c_uint64, _P, C.POINTER(C.c_int), C.POINTER(C.c_int64)]),
+    "b2_draw_epoch": (
+        _I,
+        [_P, _P, C.c_uint64, _P, _I, _I64, _I64, _P, C.POINTER(C.c_int64), C.POINTER(C.c_int),
+         C.POINTER(C.c_int64)],
+    ),
     "b2_strata_workspace_bytes": (_SZ, [_I64]),
     "b2_strata_partition": (_I, [_P, _P, _I64, _P, _I, _P, _P, _P, _P, _SZ, _P]),
     "b2_strata_partition_shards": (_I, [_P, _P, _P, _I, _P, _I, _P, _P, _P, _P, _SZ, _P]),

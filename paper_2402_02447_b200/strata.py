@@ -271,3 +271,90 @@ def draw_batch(strata: Strata, alloc: StratumAllocation, seed: int) -> list:
             pull(strata.buckets[j], take)
             short -= take
     return out
+
+
+class NativeDraws:
+    """Bit-exact native port of draw_batch (strata.py:113-161) over mutable id pools (host C++).
+
+    Same numpy PCG64 stream as the reference (SeedSequence -> PCG64 ->
+    Generator.choice(replace=False)), same swap-pop and closest-boundary
+    borrowing; differential-tested against numpy (tests/test_draws.py).  Runs
+    on the host CPU like the reference's data loader, ~100x faster than the
+    Python loop; `epoch` draws many steps in one call with the per-(key, step)
+    seeds of seeding.derive_seed.
+    """
+
+    def __init__(self, pools, boundaries):
+        import ctypes
+
+        self.lib = _lib.load(require_device=False)
+        bounds = [int(b) for b in boundaries]
+        arrs = [np.asarray(p, dtype=np.int64).reshape(-1) for p in pools]
+        if len(arrs) != len(bounds):
+            raise ValueError(f"{len(arrs)} pools for {len(bounds)} boundaries")
+        flat = np.ascontiguousarray(np.concatenate(arrs) if arrs else np.zeros(0, np.int64))
+        sizes = np.array([a.size for a in arrs], dtype=np.int64)
+        self.nstrata = len(bounds)
+        h = ctypes.c_void_p()
+        _lib.check(self.lib.b2_draws_create(ctypes.byref(h), flat.ctypes.data, sizes.ctypes.data, self.nstrata,
+                                            np.asarray(bounds, dtype=np.int64).ctypes.data))
+        self.handle = h
+
+    def remaining(self) -> tuple:
+        return tuple(int(self.lib.b2_draws_remaining(self.handle, k)) for k in range(self.nstrata))
+
+    def _raise(self, err_k, err_s):
+        raise ValueError(
+            f"stratum {err_k.value} exhausted and no other stratum can cover the remaining {err_s.value} sample(s)"
+        )
+
+    def draw(self, counts, seed: int) -> np.ndarray:
+        import ctypes
+
+        c = np.asarray(counts, dtype=np.int64)
+        if c.size != self.nstrata:
+            raise ValueError(f"allocation has {c.size} strata, corpus has {self.nstrata}")
+        out = np.empty(int(c.sum()), dtype=np.int64)
+        ek, es = ctypes.c_int(0), ctypes.c_int64(0)
+        rc = self.lib.b2_draw_batch(self.handle, c.ctypes.data, int(seed) & (2**64 - 1), out.ctypes.data,
+                                    ctypes.byref(ek), ctypes.byref(es))
+        if rc != 0:
+            self._raise(ek, es)
+        return out
+
+    def epoch(self, counts, base_seed: int, key=(), first_step: int = 0, nsteps: int = 1):
+        """Draw steps t = first_step.. with seed derive_seed(base_seed, *key, t); returns (ids[done, lb], done).
+
+        Stops early (done < nsteps) at global exhaustion; the reference would
+        raise there, callers decide.
+        """
+        import ctypes
+
+        c = np.asarray(counts, dtype=np.int64)
+        lb = int(c.sum())
+        out = np.empty((int(nsteps), lb), dtype=np.int64)
+        k = np.asarray(list(key), dtype=np.uint64)
+        done = ctypes.c_int64(0)
+        ek, es = ctypes.c_int(0), ctypes.c_int64(0)
+        self.lib.b2_draw_epoch(self.handle, c.ctypes.data, int(base_seed), k.ctypes.data if k.size else None,
+                               int(k.size), int(first_step), int(nsteps), out.ctypes.data, ctypes.byref(done),
+                               ctypes.byref(ek), ctypes.byref(es))
+        return out[: done.value], int(done.value)
+
+    def close(self) -> None:
+        if self.handle:
+            self.lib.b2_draws_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def derive_seed(seed: int, *key: int) -> int:
+    """seeding.py:18-21 (native)."""
+    lib = _lib.load(require_device=False)
+    k = np.asarray(key, dtype=np.uint64)
+    return int(lib.b2_derive_seed(int(seed), k.ctypes.data if k.size else None, int(k.size)))
