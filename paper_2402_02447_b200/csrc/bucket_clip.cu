@@ -613,7 +613,10 @@ __global__ void __launch_bounds__(AT + BT, CPS) k_bucket_clip_ws(const __grid_co
   __shared__ double redA[32], redB[32];
   __shared__ double s_coef;
   __shared__ volatile int s_bdone;  // buckets the B group has finished
-  const int G = gridDim.x, c = blockIdx.x, t = threadIdx.x;
+  // CTA groups (p.ngroups): this CTA serves buckets gid, gid+R, ... as member gr of Gc CTAs
+  const int R = p.ngroups, gid = blockIdx.x % R, gr = blockIdx.x / R;
+  const int Gc = group_size(gridDim.x, R, gid), t = threadIdx.x;
+  const int G = Gc, c = gr;
   const bool scale = p.out != nullptr;
   if (t == 0) s_bdone = 0;
   __syncthreads();
@@ -630,7 +633,7 @@ __global__ void __launch_bounds__(AT + BT, CPS) k_bucket_clip_ws(const __grid_co
     }
     group_sync<NTH>(bar);
     double v = 0.0;
-    for (int j = gt; j < G; j += NTH) v += __ldcg(&p.partials[(size_t)s * G + j]);
+    for (int j = gt; j < G; j += NTH) v += __ldcg(&p.partials[(size_t)s * kMaxGrid + j]);
     const double total = group_sum<NTH>(v, scratch, gt, bar);
     double coef = 1.0;
     if (gt == 0) {
@@ -649,11 +652,11 @@ __global__ void __launch_bounds__(AT + BT, CPS) k_bucket_clip_ws(const __grid_co
     // ================= A group: norm pass, bucket after bucket
     const int gt = t;
     const uint64_t pol_keep = scale ? l2_policy_evict_last() : l2_policy_evict_first();
-    for (int s = 0; s < p.nseg; ++s) {
-      if (scale && s > LAG) {  // L2 footprint bound: wait until B finished bucket s-LAG-1
+    for (int i = 0, s = gid; s < p.nseg; ++i, s += R) {
+      if (scale && i > LAG) {  // L2 footprint bound: wait until B finished this group's bucket i-LAG-1
         if (gt == 0) {
           unsigned ns = 32;
-          while (s_bdone < s - LAG) {
+          while (s_bdone < i - LAG) {
             __nanosleep(ns);
             if (ns < 256) ns <<= 1;
           }
@@ -728,17 +731,17 @@ __global__ void __launch_bounds__(AT + BT, CPS) k_bucket_clip_ws(const __grid_co
       if constexpr (kF64) part = __any_sync(0xffffffffu, bad) ? __longlong_as_double(0x7ff8000000000000ll) : part;
       const double tot = group_sum<AT>(part, redA, gt, kBarA);  // NaN propagates: marks inf/nan input
       if (gt == 0) {
-        p.partials[(size_t)s * G + c] = tot;
+        p.partials[(size_t)s * kMaxGrid + c] = tot;
         red_release_u32(&p.counters[s], 1u);  // fire-and-forget arrival
       }
     }
-    if (!scale)  // norm-only: publish every segment, spread over CTAs
-      for (int s = c; s < p.nseg; s += G) fold(std::integral_constant<int, AT>{}, gt, kBarA, redA, s, true);
+    if (!scale && c == 0)  // norm-only: the group's first CTA publishes its buckets
+      for (int s = gid; s < p.nseg; s += R) fold(std::integral_constant<int, AT>{}, gt, kBarA, redA, s, true);
   } else if (scale) {
     // ================= B group: scale pass, one bucket behind
     const int gt = t - AT;
     const uint64_t pol_drop = l2_policy_evict_first();
-    for (int s = 0; s < p.nseg; ++s) {
+    for (int i = 0, s = gid; s < p.nseg; ++i, s += R) {
       const double coef = fold(std::integral_constant<int, BT>{}, gt, kBarB, redB, s, c == 0);
       if (gt == 0) s_coef = coef;
       group_sync<BT>(kBarB);
@@ -784,13 +787,13 @@ __global__ void __launch_bounds__(AT + BT, CPS) k_bucket_clip_ws(const __grid_co
         for (int64_t e = e0 + gt; e < e1; e += BT) put1(out + e, static_cast<Acc>(in[e]) * cf);
       }
       group_sync<BT>(kBarB);  // whole group done with bucket s (also retires s_coef)
-      if (gt == 0) s_bdone = s + 1;
+      if (gt == 0) s_bdone = i + 1;
     }
   }
 
   __syncthreads();
   if (t == 0) {
-    if (atom_add_acq_rel_u32(&p.counters[kMaxSegs], 1u) == (unsigned)G - 1) {
+    if (atom_add_acq_rel_u32(&p.counters[kMaxSegs], 1u) == gridDim.x - 1) {
       for (int s = 0; s < p.nseg; ++s) p.counters[s] = 0u;
       p.counters[kMaxSegs] = 0u;
       __threadfence();
@@ -815,10 +818,12 @@ int launch_ws(ClipParams& p, cudaStream_t stream) {
   const int grid = (int)std::max<int64_t>(
       1, std::min<int64_t>({(int64_t)di.sm_count * std::min(CPS, occ), want, (int64_t)kMaxGrid}));
   const int N = p.seg_vec_elems;
+  p.ngroups = choose_groups(p, grid, sizeof(Tin));
   for (int s = 0; s < p.nseg; ++s) {
     Seg& sg = p.seg[s];
+    const int gs = group_size(grid, p.ngroups, s % p.ngroups);
     sg.nv = sg.vec ? (sg.n - sg.head) / N : 0;
-    sg.per = (sg.nv + grid - 1) / grid;
+    sg.per = (sg.nv + gs - 1) / gs;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -904,7 +909,8 @@ int launch_clip_k1(ClipParams& p, cudaStream_t stream) {
       default: break;
     }
   }
-  if (p.nseg >= 2) return launch_ws<Tin, Tout, 256, 256, 2, 1, 8, 4>(p, stream);
+  // norm-only launches have no scale stream: the time-sliced kernel puts every thread on the norm
+  if (p.nseg >= 2 && p.out != nullptr) return launch_ws<Tin, Tout, 256, 256, 2, 1, 8, 4>(p, stream);
   return launch_l2lag<Tin, Tout, 384, 2, 1, 8, 4, 0>(p, stream);
 }
 

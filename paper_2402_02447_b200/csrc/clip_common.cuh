@@ -33,6 +33,7 @@ struct ClipParams {
   unsigned* counters;  // [kMaxSegs + 1]; the last one is the exit counter
   int nseg;
   int seg_vec_elems;   // elements per 16 B vector (4 for f32, 2 for f64)
+  int ngroups;         // CTA groups: CTA c serves buckets s = c % ngroups (mod ngroups); 1 = whole grid
   Seg seg[kMaxSegs];
 };
 
@@ -175,6 +176,7 @@ inline int fill_params(ClipParams& p, const void* in, int in_dtype, void* out, i
   p.counters = reinterpret_cast<unsigned*>(wsb + WsLayout::counters);
   p.nseg = std::min(kMaxSegs, nseg - s0);
   p.seg_vec_elems = N;
+  p.ngroups = 1;
   for (int i = 0; i < p.nseg; ++i) {
     Seg& sg = p.seg[i];
     const int s = s0 + i;
@@ -200,6 +202,23 @@ inline int fill_params(ClipParams& p, const void* in, int in_dtype, void* out, i
   }
   return B2_OK;
 }
+
+// CTA groups for small buckets: each group of ~grid/R CTAs owns every R-th
+// bucket, so per-CTA chunks stay ~64-100 KB whatever the bucket size and the
+// grid-wide fold shrinks to a group-wide one.  R is capped so the ~2 buckets a
+// group keeps in flight (norm pass ahead of the L2 re-read) fit in L2.
+inline int choose_groups(const ClipParams& p, int grid, size_t in_elem_bytes) {
+  if (p.nseg <= 1) return 1;
+  size_t total = 0;
+  for (int s = 0; s < p.nseg; ++s) total += (size_t)p.seg[s].n * in_elem_bytes;
+  const size_t avg = total / p.nseg;
+  const size_t budget = 24u << 20;  // bytes of buckets in flight across groups (x2 for the lag)
+  int r = (int)std::max<size_t>(1, budget / std::max<size_t>(avg, 1));
+  r = std::min(r, std::max(1, grid / 4));  // >= 4 CTAs per group
+  r = std::min(r, p.nseg);
+  return r;
+}
+__host__ __device__ __forceinline__ int group_size(int grid, int r, int gid) { return (grid - gid + r - 1) / r; }
 
 }  // namespace clip
 }  // namespace b2

@@ -101,7 +101,9 @@ __global__ void __launch_bounds__(kAT + kBT + kCT, 2) k_clip_allreduce_p2p(const
   __shared__ double s_coef;
   __shared__ volatile int s_bdone;
   __shared__ uint32_t s_epoch;
-  const int G = gridDim.x, c = blockIdx.x, t = threadIdx.x;
+  // CTA groups (p.ngroups): this CTA serves buckets gid, gid+R, ... as member c of G CTAs
+  const int R = p.ngroups, gid = blockIdx.x % R;
+  const int G = group_size(gridDim.x, R, gid), c = blockIdx.x / R, t = threadIdx.x;
   if (t == 0) {
     s_bdone = 0;
     s_epoch = *f.epoch + 1u;  // read from device memory: CUDA-graph replays advance it too
@@ -113,11 +115,11 @@ __global__ void __launch_bounds__(kAT + kBT + kCT, 2) k_clip_allreduce_p2p(const
     // ================= A: norm pass (bucket s), at most 2 buckets ahead of B
     const int gt = t;
     const uint64_t pol_keep = l2_policy_evict_last();
-    for (int s = 0; s < p.nseg; ++s) {
-      if (s > 1) {
+    for (int i = 0, s = gid; s < p.nseg; ++i, s += R) {
+      if (i > 1) {
         if (gt == 0) {
           unsigned ns = 32;
-          while (s_bdone < s - 1) {
+          while (s_bdone < i - 1) {
             __nanosleep(ns);
             if (ns < 256) ns <<= 1;
           }
@@ -161,7 +163,7 @@ __global__ void __launch_bounds__(kAT + kBT + kCT, 2) k_clip_allreduce_p2p(const
       if (c == G - 1 && gt < sg.n - tail0) acc += (double)in[tail0 + gt] * in[tail0 + gt];
       const double tot = group_sum<kAT>(acc, redA, gt, kBarA);
       if (gt == 0) {
-        p.partials[(size_t)s * G + c] = tot;
+        p.partials[(size_t)s * kMaxGrid + c] = tot;
         red_release_u32(&p.counters[s], 1u);
       }
     }
@@ -170,7 +172,7 @@ __global__ void __launch_bounds__(kAT + kBT + kCT, 2) k_clip_allreduce_p2p(const
     const int gt = t - kAT;
     const uint64_t pol_drop = l2_policy_evict_first();
     __nv_bfloat16* stage = f.stage[f.rank];
-    for (int s = 0; s < p.nseg; ++s) {
+    for (int i = 0, s = gid; s < p.nseg; ++i, s += R) {
       if (gt == 0) {
         unsigned ns = 32;
         while (ld_acquire_u32(&p.counters[s]) < (unsigned)G) {
@@ -180,7 +182,7 @@ __global__ void __launch_bounds__(kAT + kBT + kCT, 2) k_clip_allreduce_p2p(const
       }
       group_sync<kBT>(kBarB);
       double v = 0.0;
-      for (int j = gt; j < G; j += kBT) v += __ldcg(&p.partials[(size_t)s * G + j]);
+      for (int j = gt; j < G; j += kBT) v += __ldcg(&p.partials[(size_t)s * kMaxGrid + j]);
       const double total = group_sum<kBT>(v, redB, gt, kBarB);
       if (gt == 0) {
         const double norm = sqrt(total);
@@ -226,20 +228,20 @@ __global__ void __launch_bounds__(kAT + kBT + kCT, 2) k_clip_allreduce_p2p(const
           __threadfence_system();
           for (int q = 0; q < f.nranks; ++q) st_release_sys(flag(f, q, 0, f.rank, s), epoch);
         }
-        s_bdone = s + 1;
+        s_bdone = i + 1;
       }
     }
   } else {
     // ================= C: two-shot allreduce of bucket s over NVLink
     const int gt = t - kAT - kBT;
-    const int R = f.nranks;
-    for (int s = 0; s < p.nseg; ++s) {
+    const int NR = f.nranks;
+    for (int s = gid; s < p.nseg; s += R) {
       if (gt == 0)
-        for (int q = 0; q < R; ++q) wait_epoch(flag(f, f.rank, 0, q, s), epoch);
+        for (int q = 0; q < NR; ++q) wait_epoch(flag(f, f.rank, 0, q, s), epoch);
       group_sync<kCT>(kBarC);
       const Seg sg = p.seg[s];
       const int64_t nv8 = sg.n / 8;                   // 16 B = 8 bf16 (host guarantees n % 8 == 0)
-      const int64_t per_r = (nv8 + R - 1) / R;
+      const int64_t per_r = (nv8 + NR - 1) / NR;
       const int64_t r0 = min64((int64_t)f.rank * per_r, nv8), r1 = min64(r0 + per_r, nv8);
       const int64_t per_c = (r1 - r0 + G - 1) / G;
       const int64_t c0 = min64(r0 + (int64_t)c * per_c, r1), c1 = min64(c0 + per_c, r1);
@@ -251,7 +253,7 @@ __global__ void __launch_bounds__(kAT + kBT + kCT, 2) k_clip_allreduce_p2p(const
           if (vi < c1) {
 #pragma unroll
             for (int q = 0; q < RMAX; ++q)
-              if (q < R) {
+              if (q < NR) {
                 const uint4* src = reinterpret_cast<const uint4*>(f.stage[q] + sg.out_off) + vi;
                 x[u][q] = CV ? __ldcv(src) : __ldcg(src);
               }
@@ -264,7 +266,7 @@ __global__ void __launch_bounds__(kAT + kBT + kCT, 2) k_clip_allreduce_p2p(const
             float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
             for (int q = 0; q < RMAX; ++q) {
-              if (q < R) {  // fixed rank order: identical bits on every rank
+              if (q < NR) {  // fixed rank order: identical bits on every rank
                 float e[8];
                 bf16x8_to_f32(x[u][q], e);
 #pragma unroll
@@ -276,7 +278,7 @@ __global__ void __launch_bounds__(kAT + kBT + kCT, 2) k_clip_allreduce_p2p(const
             const uint4 y = f32_to_bf16x8(acc);
 #pragma unroll
             for (int q = 0; q < RMAX; ++q)
-              if (q < R) __stcg(reinterpret_cast<uint4*>(f.stage[q] + sg.out_off) + vi, y);
+              if (q < NR) __stcg(reinterpret_cast<uint4*>(f.stage[q] + sg.out_off) + vi, y);
           }
         }
       }
@@ -287,18 +289,18 @@ __global__ void __launch_bounds__(kAT + kBT + kCT, 2) k_clip_allreduce_p2p(const
     group_sync<kCT>(kBarC);
     if (gt == 0) {
       __threadfence_system();
-      if (atomicAdd(&f.pcount[kMaxSegs], 1u) == (unsigned)G - 1) {
+      if (atomicAdd(&f.pcount[kMaxSegs], 1u) == gridDim.x - 1) {
         __threadfence_system();
-        for (int q = 0; q < R; ++q) st_release_sys(flag(f, q, 1, f.rank, 0), epoch);
+        for (int q = 0; q < NR; ++q) st_release_sys(flag(f, q, 1, f.rank, 0), epoch);
       }
-      if (c == 0)
-        for (int q = 0; q < R; ++q) wait_epoch(flag(f, f.rank, 1, q, 0), epoch);
+      if (blockIdx.x == 0)
+        for (int q = 0; q < NR; ++q) wait_epoch(flag(f, f.rank, 1, q, 0), epoch);
     }
   }
 
   __syncthreads();
   if (t == 0) {
-    if (atom_add_acq_rel_u32(&p.counters[kMaxSegs], 1u) == (unsigned)G - 1) {
+    if (atom_add_acq_rel_u32(&p.counters[kMaxSegs], 1u) == gridDim.x - 1) {
       for (int s = 0; s < p.nseg; ++s) {
         p.counters[s] = 0u;
         f.pcount[s] = 0u;
@@ -324,10 +326,12 @@ int launch_p2p(FusedParams& f, cudaStream_t stream) {
     B2_REQUIRE(occ >= 1, B2_ERR_CUDA, "fused kernel cannot be resident");
   }
   const int grid = std::min(di.sm_count * std::min(2, occ), kMaxGrid);
+  f.p.ngroups = choose_groups(f.p, grid, sizeof(float));
   for (int s = 0; s < f.p.nseg; ++s) {
     Seg& sg = f.p.seg[s];
+    const int gs = group_size(grid, f.p.ngroups, s % f.p.ngroups);
     sg.nv = (sg.n - sg.head) / 4;
-    sg.per = (sg.nv + grid - 1) / grid;
+    sg.per = (sg.nv + gs - 1) / gs;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
