@@ -895,7 +895,8 @@ static int clip_cfg() {
 
 // K1 configuration (tools/clip_bench.py sweeps; measurements in DESIGN.md):
 // several buckets per launch -> warp-specialised two-stream kernel
-// (256 norm + 256 scale threads, 2 CTAs/SM); a lone bucket (DDP-hook shape)
+// (192 norm + 320 scale threads, 2 CTAs/SM: the latency-bound L2 re-read
+// stream gets the larger group); a lone bucket (DDP-hook shape)
 // -> the time-sliced L2-lag kernel, which has the shorter critical path.
 // B2_CLIP_CFG overrides for A/B runs (5 = TMA ring, 10 = L2-lag, 20.. = ws).
 template <typename Tin, typename Tout>
@@ -905,12 +906,22 @@ int launch_clip_k1(ClipParams& p, cudaStream_t stream) {
       case 5: return launch_clip_tma_lag<Tin, Tout, 1, 0>(p, stream);
       case 10: return launch_l2lag<Tin, Tout, 384, 2, 1, 8, 4, 0>(p, stream);
       case 20: return launch_ws<Tin, Tout, 256, 256, 2, 1, 8, 4>(p, stream);
+      case 21: return launch_ws<Tin, Tout, 320, 192, 2, 1, 8, 4>(p, stream);
+      case 22: return launch_ws<Tin, Tout, 384, 128, 2, 1, 8, 4>(p, stream);
+      case 23: return launch_ws<Tin, Tout, 192, 320, 2, 1, 8, 4>(p, stream);
       case 24: return launch_ws<Tin, Tout, 128, 128, 4, 1, 8, 4>(p, stream);
+      case 25: return launch_ws<Tin, Tout, 256, 256, 2, 2, 8, 4>(p, stream);
+      case 26: return launch_ws<Tin, Tout, 256, 256, 2, 1, 4, 4>(p, stream);
+      case 27: return launch_ws<Tin, Tout, 160, 352, 2, 1, 8, 4>(p, stream);
+      case 28: return launch_ws<Tin, Tout, 128, 384, 2, 1, 8, 4>(p, stream);
+      case 29: return launch_ws<Tin, Tout, 224, 288, 2, 1, 8, 4>(p, stream);
+      case 30: return launch_ws<Tin, Tout, 192, 320, 2, 1, 8, 2>(p, stream);
+      case 31: return launch_ws<Tin, Tout, 192, 320, 2, 1, 12, 4>(p, stream);
       default: break;
     }
   }
   // norm-only launches have no scale stream: the time-sliced kernel puts every thread on the norm
-  if (p.nseg >= 2 && p.out != nullptr) return launch_ws<Tin, Tout, 256, 256, 2, 1, 8, 4>(p, stream);
+  if (p.nseg >= 2 && p.out != nullptr) return launch_ws<Tin, Tout, 192, 320, 2, 1, 8, 4>(p, stream);
   return launch_l2lag<Tin, Tout, 384, 2, 1, 8, 4, 0>(p, stream);
 }
 

@@ -77,7 +77,12 @@ def _to_device_matrix(workers) -> tuple[torch.Tensor, bool]:
 
 
 def _finite_or_raise(t: torch.Tensor, what: str) -> None:
-    if not bool(torch.isfinite(t).all()):
+    """Reject inf/nan (gradsync.py:189-190) with one K1 norm pass (its non-finite flags)."""
+    m = t.reshape(t.shape[0], -1) if t.ndim > 1 else t.reshape(1, -1)
+    K, D = m.shape
+    flags = torch.empty(K, dtype=torch.int32, device=m.device)
+    _clipper().clip_cast(m, None, [(k * m.stride(0), 0, D) for k in range(K)], 1.0, nonfinite=flags)
+    if bool(flags.any()):
         raise ValueError(f"{what} has non-finite components")
 
 
