@@ -131,6 +131,15 @@ int b2_bucket_clip_allreduce(b2_comm* comm, const void* in, int in_dtype, void* 
  * cross-GPU waits trap after 30 s.  nranks <= 8, nseg <= 128, buckets
  * 8-element aligned.  The workspace (b2_clip_workspace_bytes) also carries
  * the launch epoch, so the call is CUDA-graph replayable. */
+/* NVLS flavour: same contract, but the reduce of each slice is one
+ * multimem.ld_reduce (fp32 accumulate in the NVSwitch) + one multimem.st
+ * (broadcast) on `mc_stage`, the multicast address of the stage buffers
+ * (e.g. torch symmetric memory's multicast_ptr); stages are scaled by 1/N
+ * before staging so the in-switch sum is the mean. */
+int b2_bucket_clip_allreduce_nvls(const void* in, void* const* stages, void* mc_stage, uint32_t* const* flags,
+                                  int nranks, int rank, const int64_t* seg_off, const int64_t* seg_len, int nseg,
+                                  double limit, double* norms, int32_t* nonfinite, void* workspace,
+                                  size_t workspace_bytes, void* stream);
 size_t b2_p2p_flag_bytes(void);
 int b2_ipc_export(const void* dev_ptr, void* handle64, int64_t* offset);
 int b2_ipc_import(const void* handle64, int64_t offset, void** base, void** dev_ptr);

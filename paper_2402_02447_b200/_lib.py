@@ -54,6 +54,10 @@ SIGNATURES = {
         [_P, _P, C.c_uint64, _P, _I, _I64, _I64, _P, C.POINTER(C.c_int64), C.POINTER(C.c_int),
          C.POINTER(C.c_int64)],
     ),
+    "b2_bucket_clip_allreduce_nvls": (
+        _I,
+        [_P, _P, _P, _P, _I, _I, _P, _P, _I, _D, _P, _P, _P, _SZ, _P],
+    ),
     "b2_strata_workspace_bytes": (_SZ, [_I64]),
     "b2_strata_partition": (_I, [_P, _P, _I64, _P, _I, _P, _P, _P, _P, _SZ, _P]),
     "b2_strata_partition_shards": (_I, [_P, _P, _P, _I, _P, _I, _P, _P, _P, _P, _SZ, _P]),

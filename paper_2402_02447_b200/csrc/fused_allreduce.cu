@@ -44,6 +44,7 @@ struct FusedParams {
   uint32_t* flags[kMaxRanks];          // every rank's flag area [2][kMaxRanks][kMaxSegs]
   unsigned* pcount;                    // local arrival counters [2][kMaxSegs]
   unsigned* epoch;                     // launches so far (device; this launch is *epoch + 1)
+  __nv_bfloat16* mc;                   // NVLS: multicast address of the stage buffers (or null)
   int nranks, rank;
   float inv_n;
 };
@@ -92,7 +93,7 @@ __device__ __forceinline__ uint4 f32_to_bf16x8(const float (&x)[8]) {
   return v;
 }
 
-template <int kAT, int kBT, int kCT, int UA, int UB, int UC, int RMAX, int CV>
+template <int kAT, int kBT, int kCT, int UA, int UB, int UC, int RMAX, int CV, bool MC>
 __global__ void __launch_bounds__(kAT + kBT + kCT, 2) k_clip_allreduce_p2p(const __grid_constant__ FusedParams f) {
   using V = float4;
   constexpr int N = 4;
@@ -194,7 +195,8 @@ __global__ void __launch_bounds__(kAT + kBT + kCT, 2) k_clip_allreduce_p2p(const
         s_coef = coef;
       }
       group_sync<kBT>(kBarB);
-      const float cf = (float)s_coef;
+      // NVLS stages clip * 1/N: the in-switch sum of the stages is then the mean
+      const float cf = MC ? (float)(s_coef * (double)f.inv_n) : (float)s_coef;
       const Seg sg = p.seg[s];
       const float* in = static_cast<const float*>(p.in) + sg.in_off;
       __nv_bfloat16* out = stage + sg.out_off;
@@ -245,6 +247,32 @@ __global__ void __launch_bounds__(kAT + kBT + kCT, 2) k_clip_allreduce_p2p(const
       const int64_t r0 = min64((int64_t)f.rank * per_r, nv8), r1 = min64(r0 + per_r, nv8);
       const int64_t per_c = (r1 - r0 + G - 1) / G;
       const int64_t c0 = min64(r0 + (int64_t)c * per_c, r1), c1 = min64(c0 + per_c, r1);
+      if constexpr (MC) {
+        // NVSwitch reduction: one multimem load-reduce (fp32 accumulate) and one
+        // multimem store (broadcast to every rank) per 16 B
+        const char* mcb = reinterpret_cast<const char*>(f.mc + sg.out_off);
+        for (int64_t v = c0 + gt; v < c1; v += (int64_t)kCT * UC) {
+          uint32_t r[UC][4];
+#pragma unroll
+          for (int u = 0; u < UC; ++u) {
+            const int64_t vi = v + (int64_t)u * kCT;
+            if (vi < c1)
+              asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+                           : "=r"(r[u][0]), "=r"(r[u][1]), "=r"(r[u][2]), "=r"(r[u][3])
+                           : "l"(mcb + vi * 16)
+                           : "memory");
+          }
+#pragma unroll
+          for (int u = 0; u < UC; ++u) {
+            const int64_t vi = v + (int64_t)u * kCT;
+            if (vi < c1)
+              asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mcb + vi * 16),
+                           "f"(__uint_as_float(r[u][0])), "f"(__uint_as_float(r[u][1])),
+                           "f"(__uint_as_float(r[u][2])), "f"(__uint_as_float(r[u][3]))
+                           : "memory");
+          }
+        }
+      } else {
       for (int64_t v = c0 + gt; v < c1; v += (int64_t)kCT * UC) {
         uint4 x[UC][RMAX];
 #pragma unroll
@@ -282,6 +310,7 @@ __global__ void __launch_bounds__(kAT + kBT + kCT, 2) k_clip_allreduce_p2p(const
           }
         }
       }
+      }  // P2P two-shot
     }
     // one system-scope release per CTA for all of its remote stores, one
     // done flag per rank; the launch completes only once every rank's slices
@@ -313,10 +342,10 @@ __global__ void __launch_bounds__(kAT + kBT + kCT, 2) k_clip_allreduce_p2p(const
   }
 }
 
-template <int AT, int BT, int CT, int UA, int UB, int UC, int RMAX, int CV>
+template <int AT, int BT, int CT, int UA, int UB, int UC, int RMAX, int CV, bool MC = false>
 int launch_p2p(FusedParams& f, cudaStream_t stream) {
   constexpr int kAT = AT, kBT = BT, kCT = CT;
-  auto kern = k_clip_allreduce_p2p<AT, BT, CT, UA, UB, UC, RMAX, CV>;
+  auto kern = k_clip_allreduce_p2p<AT, BT, CT, UA, UB, UC, RMAX, CV, MC>;
   const DeviceInfo& di = device_info();
   B2_REQUIRE(di.coop, B2_ERR_CUDA, "device does not support cooperative launch");
   static int occ_cached[64] = {};
@@ -391,11 +420,34 @@ extern "C" int b2_ipc_close(void* base) {
   return B2_OK;
 }
 
+static int clip_allreduce_impl(const void* in, void* const* stages, void* mc_stage, uint32_t* const* flags,
+                               int nranks, int rank, const int64_t* seg_off, const int64_t* seg_len, int nseg,
+                               double limit, double* norms, int32_t* nonfinite, void* workspace,
+                               size_t workspace_bytes, void* stream);
+
+extern "C" int b2_bucket_clip_allreduce_nvls(const void* in, void* const* stages, void* mc_stage,
+                                             uint32_t* const* flags, int nranks, int rank, const int64_t* seg_off,
+                                             const int64_t* seg_len, int nseg, double limit, double* norms,
+                                             int32_t* nonfinite, void* workspace, size_t workspace_bytes,
+                                             void* stream) {
+  B2_REQUIRE(mc_stage != nullptr && reinterpret_cast<uintptr_t>(mc_stage) % 16 == 0, B2_ERR_INVALID,
+             "NVLS needs a 16 B aligned multicast address");
+  return clip_allreduce_impl(in, stages, mc_stage, flags, nranks, rank, seg_off, seg_len, nseg, limit, norms,
+                             nonfinite, workspace, workspace_bytes, stream);
+}
+
 extern "C" int b2_bucket_clip_allreduce_p2p(const void* in, void* const* stages, uint32_t* const* flags, int nranks,
-                                            int rank, const int64_t* seg_off,
-                                            const int64_t* seg_len, int nseg, double limit, double* norms,
-                                            int32_t* nonfinite, void* workspace, size_t workspace_bytes,
-                                            void* stream) {
+                                            int rank, const int64_t* seg_off, const int64_t* seg_len, int nseg,
+                                            double limit, double* norms, int32_t* nonfinite, void* workspace,
+                                            size_t workspace_bytes, void* stream) {
+  return clip_allreduce_impl(in, stages, nullptr, flags, nranks, rank, seg_off, seg_len, nseg, limit, norms,
+                             nonfinite, workspace, workspace_bytes, stream);
+}
+
+static int clip_allreduce_impl(const void* in, void* const* stages, void* mc_stage, uint32_t* const* flags,
+                               int nranks, int rank, const int64_t* seg_off, const int64_t* seg_len, int nseg,
+                               double limit, double* norms, int32_t* nonfinite, void* workspace,
+                               size_t workspace_bytes, void* stream) {
   B2_REQUIRE(in && stages && flags && seg_off && seg_len, B2_ERR_INVALID, "NULL argument");
   B2_REQUIRE(nranks >= 1 && nranks <= kMaxRanks && rank >= 0 && rank < nranks, B2_ERR_UNSUPPORTED,
              "nranks must be in [1, %d]", kMaxRanks);
@@ -423,6 +475,7 @@ extern "C" int b2_bucket_clip_allreduce_p2p(const void* in, void* const* stages,
   f.nranks = nranks;
   f.rank = rank;
   f.inv_n = 1.0f / (float)nranks;
+  f.mc = static_cast<__nv_bfloat16*>(mc_stage);
 
   // the reduce group keeps UC x RMAX 16 B vectors in flight: 32 registers
   cudaStream_t st = (cudaStream_t)stream;
@@ -431,19 +484,24 @@ extern "C" int b2_bucket_clip_allreduce_p2p(const void* in, void* const* stages,
     const char* e = getenv("B2_FUSED_CFG");
     cfg = e ? atoi(e) : 0;
   }
+  if (mc_stage) return launch_p2p<256, 128, 128, 8, 4, 4, 2, 1, true>(f, st);  // RMAX unused with NVLS
   if (nranks <= 2) {
     switch (cfg) {
       case 1: return launch_p2p<128, 128, 256, 8, 4, 4, 2, 1>(f, st);
       case 2: return launch_p2p<256, 128, 128, 8, 4, 4, 2, 0>(f, st);
-      case 3: return launch_p2p<128, 128, 256, 8, 4, 4, 2, 0>(f, st);
-      case 4: return launch_p2p<128, 64, 320, 8, 4, 4, 2, 0>(f, st);
+      case 5: return launch_p2p<192, 192, 128, 8, 4, 4, 2, 1>(f, st);
+      case 6: return launch_p2p<160, 224, 128, 8, 4, 4, 2, 1>(f, st);
+      case 7: return launch_p2p<192, 160, 160, 8, 4, 4, 2, 1>(f, st);
       default: return launch_p2p<256, 128, 128, 8, 4, 4, 2, 1>(f, st);
     }
   }
   if (nranks <= 4) {
-    if (cfg == 3 || cfg == 4) return launch_p2p<128, 128, 256, 8, 4, 2, 4, 0>(f, st);
-    return launch_p2p<256, 128, 128, 8, 4, 2, 4, 1>(f, st);
+    switch (cfg) {
+      case 5: return launch_p2p<192, 192, 128, 8, 4, 2, 4, 1>(f, st);
+      case 6: return launch_p2p<160, 224, 128, 8, 4, 2, 4, 1>(f, st);
+      case 7: return launch_p2p<192, 160, 160, 8, 4, 2, 4, 1>(f, st);
+      default: return launch_p2p<256, 128, 128, 8, 4, 2, 4, 1>(f, st);
+    }
   }
-  if (cfg == 3 || cfg == 4) return launch_p2p<128, 128, 256, 8, 4, 1, 8, 0>(f, st);
   return launch_p2p<256, 128, 128, 8, 4, 1, 8, 1>(f, st);
 }

@@ -214,6 +214,10 @@ def make_hook_state(cfg: ClipConfig, num_buckets: int, process_group=None, clip=
 class FusedBucketSync:
     """Bucket-wise clip + allreduce fused in one kernel per rank, over NVLink peer memory.
 
+    transport: "p2p" (two-shot over CUDA-IPC peer buffers), "nvls"
+    (multimem load-reduce / store on a torch symmetric-memory multicast
+    mapping: the NVSwitch sums), or "auto" (NVLS from 4 ranks up).
+
     Same contract as ``BucketwiseSync`` (rank r = worker row r, sync_bucketwise
     semantics, gradsync.py:148-162) with a bf16 comm buffer, but no NCCL: the
     clip kernel itself reduces each bucket as soon as every rank has staged it
@@ -222,7 +226,7 @@ class FusedBucketSync:
     gradient once the launch completes in stream order (graph-replayable).
     """
 
-    def __init__(self, layout: Sequence, cfg: ClipConfig, group=None, device=None):
+    def __init__(self, layout: Sequence, cfg: ClipConfig, group=None, device=None, transport: str = "auto"):
         if ClipConfig(cfg.threshold, cfg.mode).mode is not ClipMode.BUCKET_WISE:
             raise ValueError(f"config mode is {cfg.mode.value}, expected {ClipMode.BUCKET_WISE.value}")
         self.lib = _lib.load()
@@ -239,26 +243,50 @@ class FusedBucketSync:
         self.dim = self.layout[-1][1]
         stage_bytes = (self.dim * 2 + 255) // 256 * 256
         flag_bytes = self.lib.b2_p2p_flag_bytes()
-        self.buf = torch.zeros(stage_bytes + flag_bytes, dtype=torch.uint8, device=self.device)
-        self.stage = self.buf[: self.dim * 2].view(torch.bfloat16)
-        handle = (ctypes.c_char * 64)()
-        off = ctypes.c_int64()
-        _lib.check(self.lib.b2_ipc_export(self.buf.data_ptr(), handle, ctypes.byref(off)))
-        peers = [None] * self.world
-        dist.all_gather_object(peers, (bytes(handle), off.value), group=group)
+        if transport == "auto":  # NVLS cuts per-GPU traffic from 2(N-1)/N to ~(N+1)/N of a bucket: N >= 4
+            transport = "nvls" if self.world >= 4 else "p2p"
         self._opened = []
-        stages, flags = [], []
-        for q, (h, o) in enumerate(peers):
-            if q == self.rank:
-                ptr = self.buf.data_ptr()
-            else:
-                base, p = ctypes.c_void_p(), ctypes.c_void_p()
-                hb = (ctypes.c_char * 64).from_buffer_copy(h)
-                _lib.check(self.lib.b2_ipc_import(hb, o, ctypes.byref(base), ctypes.byref(p)))
-                self._opened.append(base)
-                ptr = p.value
-            stages.append(ptr)
-            flags.append(ptr + stage_bytes)
+        self.mc = 0
+        if transport == "nvls":
+            try:
+                import torch.distributed._symmetric_memory  # noqa: F401
+            except ImportError:
+                transport = "p2p"
+        self.transport = transport
+        if transport == "nvls":
+            # symmetric allocation with a multicast mapping (NVLink SHARP) via torch symmetric memory
+            import torch.distributed._symmetric_memory as symm_mem
+
+            self.buf = symm_mem.empty(stage_bytes + flag_bytes, dtype=torch.uint8, device=self.device)
+            self.buf.zero_()
+            gname = (group if group is not None else dist.group.WORLD).group_name
+            self._symm = symm_mem.rendezvous(self.buf, gname)
+            self.mc = int(self._symm.multicast_ptr)
+            if not self.mc:
+                raise RuntimeError("no multicast (NVLS) support on this system; use transport='p2p'")
+            bases = [int(x) for x in self._symm.buffer_ptrs]
+            stages = bases
+            flags = [b + stage_bytes for b in bases]
+        else:
+            self.buf = torch.zeros(stage_bytes + flag_bytes, dtype=torch.uint8, device=self.device)
+            handle = (ctypes.c_char * 64)()
+            off = ctypes.c_int64()
+            _lib.check(self.lib.b2_ipc_export(self.buf.data_ptr(), handle, ctypes.byref(off)))
+            peers = [None] * self.world
+            dist.all_gather_object(peers, (bytes(handle), off.value), group=group)
+            stages, flags = [], []
+            for q, (h, o) in enumerate(peers):
+                if q == self.rank:
+                    ptr = self.buf.data_ptr()
+                else:
+                    base, p = ctypes.c_void_p(), ctypes.c_void_p()
+                    hb = (ctypes.c_char * 64).from_buffer_copy(h)
+                    _lib.check(self.lib.b2_ipc_import(hb, o, ctypes.byref(base), ctypes.byref(p)))
+                    self._opened.append(base)
+                    ptr = p.value
+                stages.append(ptr)
+                flags.append(ptr + stage_bytes)
+        self.stage = self.buf[: self.dim * 2].view(torch.bfloat16)
         self._stages = (ctypes.c_void_p * self.world)(*stages)
         self._flags = (ctypes.c_void_p * self.world)(*flags)
         self.clipper = BucketClipper(device=self.device)
@@ -280,9 +308,15 @@ class FusedBucketSync:
         ws = self.clipper.workspace
         sp = _lib.stream_ptr(stream)
         for c0, n, offs, lens in self._chunks:
-            _lib.check(self.lib.b2_bucket_clip_allreduce_p2p(
-                grad.data_ptr(), self._stages, self._flags, self.world, self.rank, offs, lens, n,
-                float(self.limit), self._norms_call[c0:].data_ptr(), None, ws.data_ptr(), ws.numel(), sp))
+            if self.mc:
+                rc = self.lib.b2_bucket_clip_allreduce_nvls(
+                    grad.data_ptr(), self._stages, self.mc, self._flags, self.world, self.rank, offs, lens, n,
+                    float(self.limit), self._norms_call[c0:].data_ptr(), None, ws.data_ptr(), ws.numel(), sp)
+            else:
+                rc = self.lib.b2_bucket_clip_allreduce_p2p(
+                    grad.data_ptr(), self._stages, self._flags, self.world, self.rank, offs, lens, n,
+                    float(self.limit), self._norms_call[c0:].data_ptr(), None, ws.data_ptr(), ws.numel(), sp)
+            _lib.check(rc)
         return self.stage
 
     @property

@@ -43,7 +43,7 @@ def _sync_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def _fused_worker(rank, world, port, q):
+def _fused_worker(rank, world, port, q, transport="p2p"):
     import torch.distributed as dist
 
     from paper_2402_02447_b200 import ClipConfig
@@ -52,7 +52,7 @@ def _fused_worker(rank, world, port, q):
     H.init(rank, world, port, "nccl")
     try:
         g = H.worker_grad(rank, DIM8).cuda()
-        sync = FusedBucketSync(LAYOUT8, ClipConfig(1.0, "bucket_wise"))
+        sync = FusedBucketSync(LAYOUT8, ClipConfig(1.0, "bucket_wise"), transport=transport)
         outs = []
         for it in range(3):  # repeated launches exercise the epoch protocol
             outs.append(sync.sync(g).float().cpu().numpy())
@@ -198,3 +198,23 @@ def test_local_presort_nccl_matches_reference():
             if t == 0:
                 assert res[r]["step"].tolist() == per_gpu[r]
                 assert res[r]["step_tok"].tolist() == list(tok)
+
+
+def _fused_nvls_worker(rank, world, port, q):
+    _fused_worker(rank, world, port, q, transport="nvls")
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_fused_clip_allreduce_nvls_matches_reference():
+    from oracle import ddp_oracle as O
+
+    world = _world()
+    res = _run(_fused_nvls_worker, world)
+    W = np.stack([H.worker_grad(r, DIM8).double().numpy() for r in range(world)])
+    ref = O.sync_bucketwise(W, LAYOUT8, 1.0)
+    scale = np.abs(ref).max()
+    first = res[0]["outs"][0]
+    for r in range(world):
+        for out in res[r]["outs"]:
+            assert np.abs(out - ref).max() <= 2.0 ** -7 * scale
+            np.testing.assert_array_equal(out, first)  # one in-switch sum, broadcast: identical everywhere

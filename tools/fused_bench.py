@@ -25,7 +25,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--mb", type=int, default=25, help="bucket size in MiB of fp32")
-    ap.add_argument("--comm", choices=("fused", "nccl"), default="fused")
+    ap.add_argument("--comm", choices=("fused", "nvls", "nccl"), default="fused")
     args = ap.parse_args()
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -38,8 +38,9 @@ def main():
     dim = synthetic.BERT_LARGE_DIM
     g, _, _ = synthetic.bert_grads(dim, rank=rank)
     layout = B.capped_bucket_layout(dim, args.mb * 1024 * 1024 // 4)
-    if args.comm == "fused":
-        sync = FusedBucketSync(layout, B.ClipConfig(1.0, "bucket_wise"))
+    if args.comm in ("fused", "nvls"):
+        sync = FusedBucketSync(layout, B.ClipConfig(1.0, "bucket_wise"),
+                               transport="nvls" if args.comm == "nvls" else "p2p")
         fn = lambda s_: sync.sync(g, stream=s_)  # noqa: E731
     else:
         from paper_2402_02447_b200.ddp import BucketwiseSync
