@@ -213,7 +213,9 @@ def bench_clip(args, rank, world, local):
                 fused_note = f"unavailable: {str(e)[:120]}"
         if fused_replay is not None:
             step = fused_replay
-            mode = f"fused K1 + two-shot NVLink allreduce per bucket, one kernel per rank ({fused_note})"
+            mode = (f"fused K1 + allreduce per bucket over NVLink ({fsync.transport}: "
+                    f"{'NVSwitch multimem reduce' if fsync.transport == 'nvls' else 'two-shot peer memory'}), "
+                    f"one kernel per rank ({fused_note})")
             launches_per_step = 1
         else:
             step = nccl_replay
@@ -328,8 +330,8 @@ def bench_clip(args, rank, world, local):
                          "nccl_only_ms": nccl_ms, "nccl_only_busbw_gbs": bus(nccl_algbw),
                          "nccl_step_ms": nccl_step_ms, "speedup_vs_nccl_step": nccl_step_ms / ms,
                          "comm_dtype": "bf16",
-                         "collective": "fused two-shot over CUDA-IPC peer memory" if launches_per_step == 1
-                         else "ncclAllReduce avg per 25 MiB bucket, side stream"}
+                         "collective": (f"fused in K4 ({fsync.transport})" if launches_per_step == 1
+                                        else "ncclAllReduce avg per 25 MiB bucket, side stream")}
 
     # e2e: pinned host fp32 gradients -> device -> sync -> host result, through the public API
     host = torch.empty((1, dim), dtype=torch.float32, pin_memory=True)

@@ -243,30 +243,22 @@ class FusedBucketSync:
         self.dim = self.layout[-1][1]
         stage_bytes = (self.dim * 2 + 255) // 256 * 256
         flag_bytes = self.lib.b2_p2p_flag_bytes()
-        if transport == "auto":  # NVLS cuts per-GPU traffic from 2(N-1)/N to ~(N+1)/N of a bucket: N >= 4
+        auto = transport == "auto"
+        if auto:  # NVLS cuts per-GPU traffic from 2(N-1)/N to ~(N+1)/N of a bucket: N >= 4
             transport = "nvls" if self.world >= 4 else "p2p"
         self._opened = []
         self.mc = 0
         if transport == "nvls":
             try:
-                import torch.distributed._symmetric_memory  # noqa: F401
-            except ImportError:
-                transport = "p2p"
+                self._setup_nvls(group, stage_bytes, flag_bytes)
+            except Exception:
+                if not auto:
+                    raise
+                transport = "p2p"  # no multicast here: two-shot over peer memory
         self.transport = transport
         if transport == "nvls":
-            # symmetric allocation with a multicast mapping (NVLink SHARP) via torch symmetric memory
-            import torch.distributed._symmetric_memory as symm_mem
-
-            self.buf = symm_mem.empty(stage_bytes + flag_bytes, dtype=torch.uint8, device=self.device)
-            self.buf.zero_()
-            gname = (group if group is not None else dist.group.WORLD).group_name
-            self._symm = symm_mem.rendezvous(self.buf, gname)
-            self.mc = int(self._symm.multicast_ptr)
-            if not self.mc:
-                raise RuntimeError("no multicast (NVLS) support on this system; use transport='p2p'")
-            bases = [int(x) for x in self._symm.buffer_ptrs]
-            stages = bases
-            flags = [b + stage_bytes for b in bases]
+            stages = [int(x) for x in self._symm.buffer_ptrs]
+            flags = [b + stage_bytes for b in stages]
         else:
             self.buf = torch.zeros(stage_bytes + flag_bytes, dtype=torch.uint8, device=self.device)
             handle = (ctypes.c_char * 64)()
@@ -301,6 +293,19 @@ class FusedBucketSync:
         self._norms_call = torch.zeros(len(self.layout), dtype=torch.float64, device=self.device)
         torch.cuda.synchronize(self.device)
         dist.barrier(group=group)
+
+    def _setup_nvls(self, group, stage_bytes: int, flag_bytes: int) -> None:
+        """Symmetric allocation with a multicast mapping (NVLink SHARP) via torch symmetric memory."""
+        import torch.distributed._symmetric_memory as symm_mem
+
+        buf = symm_mem.empty(stage_bytes + flag_bytes, dtype=torch.uint8, device=self.device)
+        buf.zero_()
+        gname = (group if group is not None else dist.group.WORLD).group_name
+        symm = symm_mem.rendezvous(buf, gname)
+        mc = int(symm.multicast_ptr)
+        if not mc:
+            raise RuntimeError("no multicast (NVLS) support on this system; use transport='p2p'")
+        self.buf, self._symm, self.mc = buf, symm, mc
 
     def sync(self, grad: torch.Tensor, stream=None) -> torch.Tensor:
         if grad.numel() != self.dim or grad.dtype != torch.float32 or not grad.is_cuda:
