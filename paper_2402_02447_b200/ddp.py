@@ -176,11 +176,19 @@ class BucketwiseSync:
 
 class _HookState:
     def __init__(self, cfg: ClipConfig, num_buckets: int, process_group=None, clip=None):
+        self.threshold = cfg.threshold
+        self.num_buckets = num_buckets
         self.limit = cfg.threshold / math.sqrt(num_buckets)
         self.group = process_group
         self.clip = clip  # optional replacement of BucketClipper.clip_cast (CPU tests)
         self.clipper = None
         self.norms = {}
+        self.record = None  # tests: {bucket index: raw (unclipped) bucket copy}
+
+    def set_num_buckets(self, num_buckets: int) -> None:
+        """B of c/sqrt(B) (gradsync.py:155), e.g. once DDP has rebuilt its buckets."""
+        self.num_buckets = num_buckets
+        self.limit = self.threshold / math.sqrt(num_buckets)
 
 
 def bucketwise_clip_hook(state: _HookState, bucket):
@@ -198,6 +206,8 @@ def bucketwise_clip_hook(state: _HookState, bucket):
         clip = state.clipper.clip_cast
     op, post = _avg_op(state.group)
     n = buf.numel()
+    if state.record is not None:
+        state.record[bucket.index()] = buf.detach().clone()
     norm = torch.empty(1, dtype=torch.float64, device=buf.device)
     clip(buf, buf, [(0, 0, n)], state.limit, post, norm)  # in place: K1 reads before it writes
     state.norms[bucket.index()] = norm

@@ -80,9 +80,7 @@ def bert_large_step_bench(mode: str = "bucketwise", steps: int = 5, warmup: int 
     for _ in range(warmup):
         step()
     if state is not None:  # DDP rebuilt its buckets after iteration 1: fix B = c/sqrt(B)'s B
-        nb = max(state.norms) + 1 if state.norms else 1
-        state.limit = clip / math.sqrt(nb)
-        state.num_buckets = nb
+        state.set_num_buckets(max(state.norms) + 1 if state.norms else 1)
     torch.cuda.synchronize()
     dist.barrier()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

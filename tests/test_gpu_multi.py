@@ -218,3 +218,56 @@ def test_fused_clip_allreduce_nvls_matches_reference():
         for out in res[r]["outs"]:
             assert np.abs(out - ref).max() <= 2.0 ** -7 * scale
             np.testing.assert_array_equal(out, first)  # one in-switch sum, broadcast: identical everywhere
+
+
+def _hook_multi_worker(rank, world, port, q):
+    import torch.distributed as dist
+    from torch.nn.parallel import DistributedDataParallel as DDP
+
+    from paper_2402_02447_b200 import ClipConfig
+    from paper_2402_02447_b200.ddp import bucketwise_clip_hook, make_hook_state
+
+    H.init(rank, world, port, "nccl")
+    try:
+        torch.manual_seed(0)
+        model = torch.nn.Sequential(*[torch.nn.Linear(512, 512) for _ in range(6)]).cuda()  # ~1.6M params
+        ddp = DDP(model, device_ids=[rank], bucket_cap_mb=1, gradient_as_bucket_view=True)
+        state = make_hook_state(ClipConfig(0.7, "bucket_wise"), 1)
+        ddp.register_comm_hook(state, bucketwise_clip_hook)
+        torch.manual_seed(10 + rank)
+        x = torch.randn(16, 512, device="cuda") * (1.0 + 5.0 * rank)
+        ddp(x).pow(2).sum().backward()  # iteration 0: one bucket, then DDP rebuilds them
+        model.zero_grad(set_to_none=False)
+        state.norms.clear()
+        ddp(x).pow(2).sum().backward()  # iteration 1: the rebuilt buckets
+        state.set_num_buckets(max(state.norms) + 1)
+        model.zero_grad(set_to_none=False)
+        state.record = {}
+        ddp(x).pow(2).sum().backward()
+        raw = {k: v.cpu().numpy() for k, v in state.record.items()}
+        q.put((rank, {"raw": raw, "nb": state.num_buckets,
+                      "grads": torch.cat([p.grad.reshape(-1) for p in model.parameters()]).cpu().numpy()}))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_ddp_comm_hook_multi_bucket_nccl():
+    """DDP with several buckets: every parameter gradient equals mean_r clip(bucket_r, c/sqrt(B))."""
+    from oracle import ddp_oracle as O
+
+    world = _world()
+    res = _run(_hook_multi_worker, world)
+    nb = res[0]["nb"]
+    assert nb >= 3 and all(res[r]["nb"] == nb for r in range(world))
+    limit = 0.7 / np.sqrt(nb)
+    expected = {}
+    for b in range(nb):
+        rows = np.stack([res[r]["raw"][b].astype(np.float64) for r in range(world)])
+        expected[b] = O.allreduce_mean(np.stack([O.clip_by_norm(row, limit) for row in rows]))
+    # every gradient element appears in exactly one bucket: compare multisets of values per rank
+    allexp = np.sort(np.concatenate([expected[b] for b in range(nb)]))
+    for r in range(world):
+        got = np.sort(res[r]["grads"].astype(np.float64))
+        assert got.size == allexp.size
+        assert np.abs(got - allexp).max() <= 1e-5 * np.abs(allexp).max()

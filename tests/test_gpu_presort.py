@@ -253,3 +253,49 @@ def test_draws_then_presort_end_to_end(h2_golden):
             assert [s.id for s in draw_batch(st, al, seed=1000 + step)] == expect
     with pytest.raises(ValueError):
         StratumAllocation((1, 1), 3)
+
+
+def test_h2_pipeline_end_to_end_full_config():
+    """BASELINE config 1 end to end: K2 strata of 8 shards of the 10M corpus ->
+    native draws with the real per-(rank, step) seeds derive_seed(2402, r, t)
+    -> K3 deal of every node pool; equal, step by step, to the reference
+    algorithm (oracle stratify + numpy draw_batch + assign_local_presort)."""
+    from paper_2402_02447_b200 import NativeDraws
+
+    lens = synthetic_lengths()
+    shard = lens.size // 8
+    strata = stratify_shards(lens, [r * shard for r in range(9)], BOUNDS)
+    lb, steps = 48, 40
+    nat_ids, ref_pools, counts_r = [], [], []
+    for r in range(8):
+        ds = strata[r]
+        ids = ds.ids.cpu().numpy().astype(np.int64) + r * shard
+        o = np.concatenate([[0], np.cumsum(ds.counts)])
+        pools = [ids[o[k]:o[k + 1]] for k in range(4)]
+        counts = allocate_counts(ds.probs, lb).counts
+        got, done = NativeDraws(pools, BOUNDS).epoch(counts, 2402, key=(r,), nsteps=steps)
+        assert done == steps
+        nat_ids.append(got)
+        # reference: oracle strata of the shard (input order) + numpy draws
+        rp, probs = O.stratify(lens[r * shard:(r + 1) * shard], BOUNDS, ids=np.arange(r * shard, (r + 1) * shard))
+        assert probs == ds.probs
+        ref_pools.append([p.tolist() for p in rp])
+        counts_r.append(O.allocate_counts(probs, lb))
+    pool_ids = np.stack(nat_ids, axis=1).reshape(-1).astype(np.int32)  # [steps][gpu][lb]
+    pool_lens = lens[pool_ids].astype(np.int32)
+    out, tok, _, bad = presort_deal(torch.from_numpy(pool_ids).cuda(), torch.from_numpy(pool_lens).cuda(),
+                                    8 * lb, 8, "snake", max_len=512, max_id=lens.size - 1)
+    assert int(bad) == -1
+    out, tok = out.cpu().numpy(), tok.cpu().numpy()
+    for t in range(steps):
+        per_gpu_ids, per_gpu_lens = [], []
+        for r in range(8):
+            s = np.random.SeedSequence(entropy=2402, spawn_key=(r, t)).generate_state(1, np.uint64)[0]
+            d = O.draw_batch(ref_pools[r], BOUNDS, counts_r[r], int(s))
+            per_gpu_ids.append(d)
+            per_gpu_lens.append(lens[np.asarray(d)].tolist())
+        for r in range(8):
+            assert nat_ids[r][t].tolist() == per_gpu_ids[r], (r, t)
+        ref_gpu, ref_tok = O.assign_local_presort(per_gpu_ids, per_gpu_lens, 1, 8, True)
+        assert out[t].tolist() == ref_gpu, t
+        assert tok[t].tolist() == list(ref_tok), t
