@@ -72,6 +72,11 @@ __device__ __forceinline__ void wait_epoch(const uint32_t* p, uint32_t epoch) {
     if (global_ns() - t0 > kSpinTimeoutNs) __trap();  // a peer never arrived: fail, do not hang
   }
 }
+// timeline stamps (ns) in the unused partial rows kMaxSegs-1-k of the
+// workspace, read back by tools/k4_timeline.py (only when nseg leaves them free)
+__device__ __forceinline__ void stamp(const ClipParams& p, int k) {
+  if (p.nseg <= kMaxSegs - 8) reinterpret_cast<uint64_t*>(p.partials)[(size_t)(kMaxSegs - 1 - k) * kMaxGrid + blockIdx.x] = global_ns();
+}
 __device__ __forceinline__ uint32_t* flag(const FusedParams& f, int owner, int kind, int src, int s) {
   return f.flags[owner] + ((size_t)kind * kMaxRanks + src) * kMaxSegs + s;
 }
@@ -93,7 +98,16 @@ __device__ __forceinline__ uint4 f32_to_bf16x8(const float (&x)[8]) {
   return v;
 }
 
-template <int kAT, int kBT, int kCT, int UA, int UB, int UC, int RMAX, int CV, bool MC>
+__device__ __forceinline__ uint32_t ld_acquire_cta_shared(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"((uint32_t)__cvta_generic_to_shared(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta_shared(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(p)), "r"(v) : "memory");
+}
+
+template <int kAT, int kBT, int kCT, int UA, int UB, int UC, int RMAX, int CV, bool MC, bool FLAT, int THR>
 __global__ void __launch_bounds__(kAT + kBT + kCT, 2) k_clip_allreduce_p2p(const __grid_constant__ FusedParams f) {
   using V = float4;
   constexpr int N = 4;
@@ -101,16 +115,19 @@ __global__ void __launch_bounds__(kAT + kBT + kCT, 2) k_clip_allreduce_p2p(const
   __shared__ double redA[32], redB[32];
   __shared__ double s_coef;
   __shared__ volatile int s_bdone;
+  __shared__ volatile int s_cprog;  // FLAT: the bucket (local index) C is working on
   __shared__ uint32_t s_epoch;
   // CTA groups (p.ngroups): this CTA serves buckets gid, gid+R, ... as member c of G CTAs
   const int R = p.ngroups, gid = blockIdx.x % R;
   const int G = group_size(gridDim.x, R, gid), c = blockIdx.x / R, t = threadIdx.x;
   if (t == 0) {
     s_bdone = 0;
+    s_cprog = 0;
     s_epoch = *f.epoch + 1u;  // read from device memory: CUDA-graph replays advance it too
   }
   __syncthreads();
   const uint32_t epoch = s_epoch;
+  if (t == 0) stamp(p, 0);
 
   if (t < kAT) {
     // ================= A: norm pass (bucket s), at most 2 buckets ahead of B
@@ -176,6 +193,15 @@ __global__ void __launch_bounds__(kAT + kBT + kCT, 2) k_clip_allreduce_p2p(const
     for (int i = 0, s = gid; s < p.nseg; ++i, s += R) {
       if (gt == 0) {
         unsigned ns = 32;
+        if constexpr (FLAT && THR > 0) {
+          // the clip only has to stay ahead of the NVLink-bound reduce: running
+          // further ahead just competes with it for HBM and issue slots
+          while (i > s_cprog + THR) {
+            __nanosleep(ns);
+            if (ns < 256) ns <<= 1;
+          }
+          ns = 32;
+        }
         while (ld_acquire_u32(&p.counters[s]) < (unsigned)G) {
           __nanosleep(ns);
           if (ns < 256) ns <<= 1;
@@ -232,6 +258,118 @@ __global__ void __launch_bounds__(kAT + kBT + kCT, 2) k_clip_allreduce_p2p(const
         }
         s_bdone = i + 1;
       }
+    }
+    if (gt == 0) stamp(p, 1);
+  } else if constexpr (FLAT) {
+    // ================= C (flat): this CTA's slices of all its buckets as ONE
+    // stream — no per-bucket barrier or ragged tail; a bucket's ready flags
+    // are acquired by the first thread that reaches it and cached in smem
+    const int gt = t - kAT - kBT;
+    const int NR = f.nranks;
+    __shared__ int64_t s_beg[kMaxSegs + 1], s_voff[kMaxSegs];
+    __shared__ uint32_t s_rdy[kMaxSegs];
+    __shared__ int s_sid[kMaxSegs];
+    int nb = 0;
+    for (int s = gid; s < p.nseg; s += R) ++nb;
+    if (gt == 0) {
+      int64_t acc = 0;
+      for (int i = 0; i < nb; ++i) {
+        const int s = gid + i * R;
+        const Seg sg = p.seg[s];
+        const int64_t nv8 = sg.n / 8;
+        const int64_t per_r = (nv8 + NR - 1) / NR;
+        const int64_t r0 = min64((int64_t)f.rank * per_r, nv8), r1 = min64(r0 + per_r, nv8);
+        const int64_t per_c = (r1 - r0 + G - 1) / G;
+        const int64_t c0 = min64(r0 + (int64_t)c * per_c, r1), c1 = min64(c0 + per_c, r1);
+        s_beg[i] = acc;
+        s_voff[i] = sg.out_off / 8 + c0 - acc;  // stage vector index = flat index + s_voff
+        s_sid[i] = s;
+        s_rdy[i] = 0u;
+        acc += c1 - c0;
+      }
+      s_beg[nb] = acc;
+    }
+    group_sync<kCT>(kBarC);
+    const int64_t M = s_beg[nb];
+    int cur = 0;
+    for (int64_t f0 = gt; f0 < M; f0 += (int64_t)kCT * UC) {
+      uint4 x[UC][RMAX];
+      int64_t vix[UC];
+#pragma unroll
+      for (int u = 0; u < UC; ++u) {
+        const int64_t fi = f0 + (int64_t)u * kCT;
+        vix[u] = -1;
+        if (fi < M) {
+          while (fi >= s_beg[cur + 1]) {
+            ++cur;
+            if (THR > 0 && gt == 0) s_cprog = cur;
+          }
+          if (ld_acquire_cta_shared(&s_rdy[cur]) == 0u) {
+            for (int q = 0; q < NR; ++q) wait_epoch(flag(f, f.rank, 0, q, s_sid[cur]), epoch);
+            st_release_cta_shared(&s_rdy[cur], 1u);
+            if (cur == 0 && gt == 0) stamp(p, 2);
+          }
+          vix[u] = fi + s_voff[cur];
+          if constexpr (MC) {
+            // NVSwitch sums the N stages (fp32 accumulate; the stages hold clip/N)
+            asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(x[u][0].x), "=r"(x[u][0].y), "=r"(x[u][0].z), "=r"(x[u][0].w)
+                         : "l"(reinterpret_cast<const uint4*>(f.mc) + vix[u])
+                         : "memory");
+          } else {
+#pragma unroll
+            for (int q = 0; q < RMAX; ++q)
+              if (q < NR) {
+                const uint4* src = reinterpret_cast<const uint4*>(f.stage[q]) + vix[u];
+                x[u][q] = CV ? __ldcv(src) : __ldcg(src);
+              }
+          }
+        }
+      }
+      if constexpr (MC) {
+#pragma unroll
+        for (int u = 0; u < UC; ++u)
+          if (vix[u] >= 0)  // one store, multicast to every rank's stage
+            asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(
+                             reinterpret_cast<uint4*>(f.mc) + vix[u]),
+                         "f"(__uint_as_float(x[u][0].x)), "f"(__uint_as_float(x[u][0].y)),
+                         "f"(__uint_as_float(x[u][0].z)), "f"(__uint_as_float(x[u][0].w))
+                         : "memory");
+      } else {
+#pragma unroll
+      for (int u = 0; u < UC; ++u) {
+        if (vix[u] >= 0) {
+          float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int q = 0; q < RMAX; ++q) {
+            if (q < NR) {  // fixed rank order: identical bits on every rank
+              float e[8];
+              bf16x8_to_f32(x[u][q], e);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) acc[i] += e[i];
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[i] *= f.inv_n;  // mean, not sum (gradsync.py:128)
+          const uint4 y = f32_to_bf16x8(acc);
+#pragma unroll
+          for (int q = 0; q < RMAX; ++q)
+            if (q < NR) __stcg(reinterpret_cast<uint4*>(f.stage[q]) + vix[u], y);
+        }
+      }
+      }  // P2P
+    }
+    if (THR > 0 && gt == 0) s_cprog = nb;
+    group_sync<kCT>(kBarC);
+    if (gt == 0) stamp(p, 3);
+    if (gt == 0) {
+      __threadfence_system();
+      if (atomicAdd(&f.pcount[kMaxSegs], 1u) == gridDim.x - 1) {
+        __threadfence_system();
+        for (int q = 0; q < NR; ++q) st_release_sys(flag(f, q, 1, f.rank, 0), epoch);
+      }
+      if (blockIdx.x == 0)
+        for (int q = 0; q < NR; ++q) wait_epoch(flag(f, f.rank, 1, q, 0), epoch);
     }
   } else {
     // ================= C: two-shot allreduce of bucket s over NVLink
@@ -329,6 +467,7 @@ __global__ void __launch_bounds__(kAT + kBT + kCT, 2) k_clip_allreduce_p2p(const
 
   __syncthreads();
   if (t == 0) {
+    stamp(p, 4);
     if (atom_add_acq_rel_u32(&p.counters[kMaxSegs], 1u) == gridDim.x - 1) {
       for (int s = 0; s < p.nseg; ++s) {
         p.counters[s] = 0u;
@@ -342,10 +481,11 @@ __global__ void __launch_bounds__(kAT + kBT + kCT, 2) k_clip_allreduce_p2p(const
   }
 }
 
-template <int AT, int BT, int CT, int UA, int UB, int UC, int RMAX, int CV, bool MC = false>
+template <int AT, int BT, int CT, int UA, int UB, int UC, int RMAX, int CV, bool MC = false, bool FLAT = false,
+          int THR = 0>
 int launch_p2p(FusedParams& f, cudaStream_t stream) {
   constexpr int kAT = AT, kBT = BT, kCT = CT;
-  auto kern = k_clip_allreduce_p2p<AT, BT, CT, UA, UB, UC, RMAX, CV, MC>;
+  auto kern = k_clip_allreduce_p2p<AT, BT, CT, UA, UB, UC, RMAX, CV, MC, FLAT, THR>;
   const DeviceInfo& di = device_info();
   B2_REQUIRE(di.coop, B2_ERR_CUDA, "device does not support cooperative launch");
   static int occ_cached[64] = {};
@@ -484,7 +624,14 @@ static int clip_allreduce_impl(const void* in, void* const* stages, void* mc_sta
     const char* e = getenv("B2_FUSED_CFG");
     cfg = e ? atoi(e) : 0;
   }
-  if (mc_stage) return launch_p2p<256, 128, 128, 8, 4, 4, 2, 1, true>(f, st);  // RMAX unused with NVLS
+  if (mc_stage) {  // RMAX 1: one multimem load per vector
+    switch (cfg) {
+      case 1: return launch_p2p<256, 128, 128, 8, 4, 4, 1, 1, true>(f, st);
+      case 2: return launch_p2p<128, 256, 128, 8, 4, 8, 1, 1, true, true>(f, st);
+      case 3: return launch_p2p<128, 256, 128, 8, 4, 16, 1, 1, true, true>(f, st);
+      default: return launch_p2p<128, 256, 128, 8, 4, 8, 1, 1, true, true>(f, st);
+    }
+  }
   if (nranks <= 2) {
     switch (cfg) {
       case 1: return launch_p2p<128, 128, 256, 8, 4, 4, 2, 1>(f, st);
@@ -492,7 +639,17 @@ static int clip_allreduce_impl(const void* in, void* const* stages, void* mc_sta
       case 5: return launch_p2p<192, 192, 128, 8, 4, 4, 2, 1>(f, st);
       case 6: return launch_p2p<160, 224, 128, 8, 4, 4, 2, 1>(f, st);
       case 7: return launch_p2p<192, 160, 160, 8, 4, 4, 2, 1>(f, st);
-      default: return launch_p2p<256, 128, 128, 8, 4, 4, 2, 1>(f, st);
+      case 10: return launch_p2p<256, 128, 128, 8, 4, 4, 2, 1, false, true>(f, st);
+      case 11: return launch_p2p<256, 128, 128, 8, 4, 8, 2, 1, false, true>(f, st);
+      case 12: return launch_p2p<256, 128, 128, 8, 4, 4, 2, 0, false, true>(f, st);
+      case 13: return launch_p2p<192, 160, 160, 8, 4, 4, 2, 1, false, true>(f, st);
+      case 18: return launch_p2p<192, 192, 128, 8, 4, 8, 2, 1, false, true>(f, st);
+      case 19: return launch_p2p<128, 256, 128, 8, 4, 8, 2, 1, false, true>(f, st);
+      case 20: return launch_p2p<256, 128, 128, 8, 8, 8, 2, 1, false, true>(f, st);
+      case 21: return launch_p2p<192, 192, 128, 8, 8, 8, 2, 1, false, true>(f, st);
+      case 22: return launch_p2p<160, 224, 128, 8, 4, 8, 2, 1, false, true>(f, st);
+      case 9: return launch_p2p<256, 128, 128, 8, 4, 4, 2, 1>(f, st);  // per-bucket C (round-1 v1)
+      default: return launch_p2p<128, 256, 128, 8, 4, 8, 2, 1, false, true>(f, st);
     }
   }
   if (nranks <= 4) {
@@ -500,8 +657,14 @@ static int clip_allreduce_impl(const void* in, void* const* stages, void* mc_sta
       case 5: return launch_p2p<192, 192, 128, 8, 4, 2, 4, 1>(f, st);
       case 6: return launch_p2p<160, 224, 128, 8, 4, 2, 4, 1>(f, st);
       case 7: return launch_p2p<192, 160, 160, 8, 4, 2, 4, 1>(f, st);
-      default: return launch_p2p<256, 128, 128, 8, 4, 2, 4, 1>(f, st);
+      case 10: return launch_p2p<256, 128, 128, 8, 4, 2, 4, 1, false, true>(f, st);
+      case 11: return launch_p2p<256, 128, 128, 8, 4, 4, 4, 1, false, true>(f, st);
+      case 12: return launch_p2p<128, 256, 128, 8, 4, 4, 4, 1, false, true>(f, st);
+      case 13: return launch_p2p<192, 192, 128, 8, 4, 4, 4, 1, false, true>(f, st);
+      case 14: return launch_p2p<128, 256, 128, 8, 4, 2, 4, 1, false, true>(f, st);
+      case 9: return launch_p2p<256, 128, 128, 8, 4, 2, 4, 1>(f, st);  // per-bucket C (round-1 v1)
+      default: return launch_p2p<128, 256, 128, 8, 4, 4, 4, 1, false, true>(f, st);
     }
   }
-  return launch_p2p<256, 128, 128, 8, 4, 1, 8, 1>(f, st);
+  return launch_p2p<128, 256, 128, 8, 4, 2, 8, 1, false, true>(f, st);
 }
