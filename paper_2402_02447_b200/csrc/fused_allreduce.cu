@@ -6,23 +6,29 @@
 // no norm collective), then averaged over workers (allreduce_mean, :119-128).
 //
 // Every rank owns a symmetric bf16 stage buffer (the comm buffer) mapped into
-// every peer (CUDA IPC).  Three warp groups per CTA, 2 CTAs per SM:
-//   A (256 thr): norm pass of bucket s (128-bit loads, L2 evict_last), one
-//                fp64 partial per (bucket, CTA), fire-and-forget;
-//   B (128 thr): bucket s-1: fixed-order fold -> coefficient, L2 re-read,
-//                scale, cast, store into the LOCAL stage; the last CTA to
-//                finish raises ready[rank][s] in every peer's flag area;
-//   C (128 thr): two-shot allreduce of bucket s: once every rank's bucket s is
-//                staged, this rank reduces its 1/N slice — 16 B loads from all
-//                N stages (peer loads go over NVLink), fp32 sum in rank order,
-//                x 1/N, bf16 — and stores the result into all N stages; after
-//                the last bucket one system-scope release per CTA, and the
-//                last CTA raises done[rank] everywhere.
-// The launch ends when this rank has seen every done flag, so the local stage
-// then holds the averaged clipped gradient.  Per-rank NVLink traffic per
-// bucket is (N-1)/N of it in and out — the ring's volume without its
-// 2(N-1) latency steps.  Flags carry a per-launch epoch (no resets); every
-// cross-GPU wait is bounded (trap after 30 s instead of a hang).
+// every peer (CUDA IPC, or one NVLS multicast object).  One persistent
+// cooperative kernel per GPU, 2 CTAs per SM, roles split BY SM:
+//   clip CTAs (SMs >= comm_sms), K1's two warp-specialised streams:
+//     A (192 thr): norm pass of bucket s (128-bit loads, L2 evict_last), one
+//                  fp64 partial per (bucket, CTA), fire-and-forget;
+//     B (320 thr): fixed-order fold -> coefficient, L2 re-read, scale, cast,
+//                  store into the LOCAL stage; the group's last CTA publishes
+//                  "bucket s staged" with a gpu-scope release of this rank's
+//                  own ready flag;
+//   comm CTAs (SMs < comm_sms): one warp forwards ready flags (system fence,
+//     then a sys-scope release into every peer's flag area); the other 15
+//     warps reduce this rank's 1/N slice of every bucket, as one continuous
+//     stream, once every rank has staged it — 16 B loads from all N stages
+//     (peer loads go over NVLink), fp32 sum in rank order, x 1/N, bf16, and a
+//     store into all N stages (P2P two-shot); or one multimem load-reduce and
+//     one multimem store (NVLS: the switch sums).
+// Why by SM: remote loads on an SM starve that SM's own HBM stream
+// (tools/mb/contention_mb.cu), and a system-scope fence on the clip's
+// per-bucket path costs 30+ µs under NVLink load; both measured, both moved
+// off the clip SMs.  The launch ends when this rank has seen every rank's done
+// flag, so the local stage then holds the averaged clipped gradient.  Flags
+// carry a per-launch epoch (no resets); every cross-GPU wait is bounded (trap
+// after 30 s instead of a hang).
 #include "clip_common.cuh"
 
 #include <cuda_bf16.h>
@@ -35,7 +41,7 @@ namespace {
 using namespace clip;
 
 constexpr int kMaxRanks = 8;
-constexpr int kBarA = 1, kBarB = 2, kBarC = 3;
+constexpr int kBarA = 1, kBarB = 2;
 constexpr uint64_t kSpinTimeoutNs = 30ull * 1000 * 1000 * 1000;
 
 struct FusedParams {
@@ -47,6 +53,7 @@ struct FusedParams {
   __nv_bfloat16* mc;                   // NVLS: multicast address of the stage buffers (or null)
   int nranks, rank;
   float inv_n;
+  int comm_sms;  // split kernel: CTAs on SMs [0, comm_sms) reduce, all others clip
 };
 
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
@@ -56,6 +63,9 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
 }
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ uint64_t global_ns() {
   uint64_t t;
@@ -107,211 +117,234 @@ __device__ __forceinline__ void st_release_cta_shared(uint32_t* p, uint32_t v) {
   asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(p)), "r"(v) : "memory");
 }
 
-template <int kAT, int kBT, int kCT, int UA, int UB, int UC, int RMAX, int CV, bool MC, bool FLAT, int THR>
-__global__ void __launch_bounds__(kAT + kBT + kCT, 2) k_clip_allreduce_p2p(const __grid_constant__ FusedParams f) {
+__device__ __forceinline__ unsigned smid_u32() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// Split-role K4: remote (NVLink) loads on an SM starve that SM's own HBM
+// stream (tools/mb/contention_mb.cu: local reads fall from 6.9 to 1.4 TB/s
+// when 4 of 16 warps pull from a peer; they keep 6.6 TB/s when the pulls run
+// on 16 other SMs).  So the roles are split by SM, not by warp: CTAs resident
+// on SMs [0, comm_sms) only reduce (all their threads), every other CTA only
+// clips (A norm stream ∥ B scale stream, K1's split).  Roles and their counts
+// are settled by one registration barrier at entry (the launch is
+// cooperative, so every CTA is resident); chunks are derived from the actual
+// counts on the device.
+template <int kAT, int kBT, int UA, int UB, int UC, int RMAX, bool MC>
+__global__ void __launch_bounds__(kAT + kBT, 2) k_clip_allreduce_split(const __grid_constant__ FusedParams f) {
   using V = float4;
-  constexpr int N = 4;
+  constexpr int N = 4, kT = kAT + kBT;
   const ClipParams& p = f.p;
   __shared__ double redA[32], redB[32];
   __shared__ double s_coef;
   __shared__ volatile int s_bdone;
-  __shared__ volatile int s_cprog;  // FLAT: the bucket (local index) C is working on
   __shared__ uint32_t s_epoch;
-  // CTA groups (p.ngroups): this CTA serves buckets gid, gid+R, ... as member c of G CTAs
-  const int R = p.ngroups, gid = blockIdx.x % R;
-  const int G = group_size(gridDim.x, R, gid), c = blockIdx.x / R, t = threadIdx.x;
+  __shared__ int s_role, s_idx, s_nk, s_nc;
+  const int t = threadIdx.x;
+  unsigned* reg = f.pcount + kMaxSegs + 1;  // [0] clip CTAs, [1] comm CTAs, [2] arrivals
   if (t == 0) {
     s_bdone = 0;
-    s_cprog = 0;
-    s_epoch = *f.epoch + 1u;  // read from device memory: CUDA-graph replays advance it too
+    s_epoch = *f.epoch + 1u;
+    const int role = (int)smid_u32() < f.comm_sms ? 1 : 0;
+    s_role = role;
+    s_idx = (int)atomicAdd(&reg[role], 1u);
+    red_release_u32(&reg[2], 1u);
+    const uint64_t t0 = global_ns();
+    while (ld_acquire_u32(&reg[2]) < gridDim.x)
+      if (global_ns() - t0 > kSpinTimeoutNs) __trap();
+    s_nk = (int)ld_acquire_u32(&reg[0]);
+    s_nc = (int)ld_acquire_u32(&reg[1]);
+    if (s_nk == 0 || s_nc == 0) __trap();  // host sizes comm_sms inside the SM count
+    stamp(p, 0);
   }
   __syncthreads();
   const uint32_t epoch = s_epoch;
-  if (t == 0) stamp(p, 0);
+  const int NR = f.nranks;
 
-  if (t < kAT) {
-    // ================= A: norm pass (bucket s), at most 2 buckets ahead of B
-    const int gt = t;
-    const uint64_t pol_keep = l2_policy_evict_last();
-    for (int i = 0, s = gid; s < p.nseg; ++i, s += R) {
-      if (i > 1) {
+  if (s_role == 0) {
+    // ============================ clip CTA: A (norm) ∥ B (scale into the stage)
+    const int R = p.ngroups, kidx = s_idx, gid = kidx % R;
+    const int G = group_size(s_nk, R, gid), c = kidx / R;
+    if (t < kAT) {
+      const int gt = t;
+      const uint64_t pol_keep = l2_policy_evict_last();
+      for (int i = 0, s = gid; s < p.nseg; ++i, s += R) {
+        if (i > 1) {
+          if (gt == 0) {
+            unsigned ns = 32;
+            while (s_bdone < i - 1) {
+              __nanosleep(ns);
+              if (ns < 256) ns <<= 1;
+            }
+          }
+          group_sync<kAT>(kBarA);
+        }
+        const Seg sg = p.seg[s];
+        const float* in = static_cast<const float*>(p.in) + sg.in_off;
+        const int64_t per = (sg.nv + G - 1) / G;
+        double acc = 0.0;
+        const V* vin = reinterpret_cast<const V*>(in + sg.head);
+        const int64_t v0 = min64((int64_t)c * per, sg.nv), v1 = min64(v0 + per, sg.nv);
+        for (int64_t v = v0 + gt; v < v1; v += (int64_t)kAT * UA) {
+          V x[UA];
+#pragma unroll
+          for (int u = 0; u < UA; ++u) {
+            const int64_t vi = v + (int64_t)u * kAT;
+            x[u] = vi < v1 ? ld_a<0>(vin + vi, pol_keep) : V{};
+          }
+          float m = 0.0f;
+          unsigned nz = 0;
+#pragma unroll
+          for (int u = 0; u < UA; ++u) {
+            m = fmaf(x[u].x, x[u].x, m);
+            m = fmaf(x[u].y, x[u].y, m);
+            m = fmaf(x[u].z, x[u].z, m);
+            m = fmaf(x[u].w, x[u].w, m);
+            nz |= __float_as_uint(x[u].x) | __float_as_uint(x[u].y) | __float_as_uint(x[u].z) | __float_as_uint(x[u].w);
+          }
+          if (m >= 0x1p-100f && m <= 0x1p100f) {
+            acc += (double)m;
+          } else if ((nz << 1) != 0u) {  // out-of-range mini-sum: exact fp64
+#pragma unroll
+            for (int u = 0; u < UA; ++u)
+              acc += (double)x[u].x * x[u].x + (double)x[u].y * x[u].y + (double)x[u].z * x[u].z +
+                     (double)x[u].w * x[u].w;
+          }
+        }
+        const int64_t tail0 = sg.head + sg.nv * N;
+        if (c == 0 && gt < sg.head) acc += (double)in[gt] * in[gt];
+        if (c == G - 1 && gt < sg.n - tail0) acc += (double)in[tail0 + gt] * in[tail0 + gt];
+        const double tot = group_sum<kAT>(acc, redA, gt, kBarA);
+        if (gt == 0) {
+          p.partials[(size_t)s * kMaxGrid + c] = tot;
+          red_release_u32(&p.counters[s], 1u);
+        }
+      }
+    } else {
+      const int gt = t - kAT;
+      const uint64_t pol_drop = l2_policy_evict_first();
+      __nv_bfloat16* stage = f.stage[f.rank];
+      for (int i = 0, s = gid; s < p.nseg; ++i, s += R) {
         if (gt == 0) {
           unsigned ns = 32;
-          while (s_bdone < i - 1) {
+          while (ld_acquire_u32(&p.counters[s]) < (unsigned)G) {
             __nanosleep(ns);
             if (ns < 256) ns <<= 1;
           }
         }
-        group_sync<kAT>(kBarA);
-      }
-      const Seg sg = p.seg[s];
-      const float* in = static_cast<const float*>(p.in) + sg.in_off;
-      double acc = 0.0;
-      const V* vin = reinterpret_cast<const V*>(in + sg.head);
-      const int64_t v0 = min64((int64_t)c * sg.per, sg.nv), v1 = min64(v0 + sg.per, sg.nv);
-      for (int64_t v = v0 + gt; v < v1; v += (int64_t)kAT * UA) {
-        V x[UA];
-#pragma unroll
-        for (int u = 0; u < UA; ++u) {
-          const int64_t vi = v + (int64_t)u * kAT;
-          x[u] = vi < v1 ? ld_a<0>(vin + vi, pol_keep) : V{};
-        }
-        // fp32 mini-sum of <= 4*UA squares promoted to fp64; out-of-range -> exact fp64
-        float m = 0.0f;
-        unsigned nz = 0;
-#pragma unroll
-        for (int u = 0; u < UA; ++u) {
-          m = fmaf(x[u].x, x[u].x, m);
-          m = fmaf(x[u].y, x[u].y, m);
-          m = fmaf(x[u].z, x[u].z, m);
-          m = fmaf(x[u].w, x[u].w, m);
-          nz |= __float_as_uint(x[u].x) | __float_as_uint(x[u].y) | __float_as_uint(x[u].z) | __float_as_uint(x[u].w);
-        }
-        if (m >= 0x1p-100f && m <= 0x1p100f) {
-          acc += (double)m;
-        } else if ((nz << 1) != 0u) {
-#pragma unroll
-          for (int u = 0; u < UA; ++u)
-            acc += (double)x[u].x * x[u].x + (double)x[u].y * x[u].y + (double)x[u].z * x[u].z +
-                   (double)x[u].w * x[u].w;
-        }
-      }
-      const int64_t tail0 = sg.head + sg.nv * N;
-      if (c == 0 && gt < sg.head) acc += (double)in[gt] * in[gt];
-      if (c == G - 1 && gt < sg.n - tail0) acc += (double)in[tail0 + gt] * in[tail0 + gt];
-      const double tot = group_sum<kAT>(acc, redA, gt, kBarA);
-      if (gt == 0) {
-        p.partials[(size_t)s * kMaxGrid + c] = tot;
-        red_release_u32(&p.counters[s], 1u);
-      }
-    }
-  } else if (t < kAT + kBT) {
-    // ================= B: coefficient + scale + cast into the local stage
-    const int gt = t - kAT;
-    const uint64_t pol_drop = l2_policy_evict_first();
-    __nv_bfloat16* stage = f.stage[f.rank];
-    for (int i = 0, s = gid; s < p.nseg; ++i, s += R) {
-      if (gt == 0) {
-        unsigned ns = 32;
-        if constexpr (FLAT && THR > 0) {
-          // the clip only has to stay ahead of the NVLink-bound reduce: running
-          // further ahead just competes with it for HBM and issue slots
-          while (i > s_cprog + THR) {
-            __nanosleep(ns);
-            if (ns < 256) ns <<= 1;
+        group_sync<kBT>(kBarB);
+        double v = 0.0;
+        for (int j = gt; j < G; j += kBT) v += __ldcg(&p.partials[(size_t)s * kMaxGrid + j]);
+        const double total = group_sum<kBT>(v, redB, gt, kBarB);
+        if (gt == 0) {
+          const double norm = sqrt(total);
+          const double coef = (norm >= p.limit) ? p.limit / norm : 1.0;  // gradsync.py:114-116
+          if (c == 0) {
+            if (p.norms) p.norms[s] = norm;
+            if (p.nonfinite) p.nonfinite[s] = !isfinite(total) ? 1 : 0;
           }
-          ns = 32;
+          s_coef = coef;
         }
-        while (ld_acquire_u32(&p.counters[s]) < (unsigned)G) {
-          __nanosleep(ns);
-          if (ns < 256) ns <<= 1;
-        }
-      }
-      group_sync<kBT>(kBarB);
-      double v = 0.0;
-      for (int j = gt; j < G; j += kBT) v += __ldcg(&p.partials[(size_t)s * kMaxGrid + j]);
-      const double total = group_sum<kBT>(v, redB, gt, kBarB);
-      if (gt == 0) {
-        const double norm = sqrt(total);
-        const double coef = (norm >= p.limit) ? p.limit / norm : 1.0;  // gradsync.py:114-116
-        if (c == 0) {
-          if (p.norms) p.norms[s] = norm;
-          if (p.nonfinite) p.nonfinite[s] = !isfinite(total) ? 1 : 0;
-        }
-        s_coef = coef;
-      }
-      group_sync<kBT>(kBarB);
-      // NVLS stages clip * 1/N: the in-switch sum of the stages is then the mean
-      const float cf = MC ? (float)(s_coef * (double)f.inv_n) : (float)s_coef;
-      const Seg sg = p.seg[s];
-      const float* in = static_cast<const float*>(p.in) + sg.in_off;
-      __nv_bfloat16* out = stage + sg.out_off;
-      const V* vin = reinterpret_cast<const V*>(in + sg.head);
-      const int64_t v0 = min64((int64_t)c * sg.per, sg.nv), v1 = min64(v0 + sg.per, sg.nv);
-      for (int64_t v = v0 + gt; v < v1; v += (int64_t)kBT * UB) {
-        V x[UB];
+        group_sync<kBT>(kBarB);
+        const float cf = MC ? (float)(s_coef * (double)f.inv_n) : (float)s_coef;
+        const Seg sg = p.seg[s];
+        const float* in = static_cast<const float*>(p.in) + sg.in_off;
+        __nv_bfloat16* out = stage + sg.out_off;
+        const V* vin = reinterpret_cast<const V*>(in + sg.head);
+        const int64_t per = (sg.nv + G - 1) / G;
+        const int64_t v0 = min64((int64_t)c * per, sg.nv), v1 = min64(v0 + per, sg.nv);
+        for (int64_t v = v0 + gt; v < v1; v += (int64_t)kBT * UB) {
+          V x[UB];
 #pragma unroll
-        for (int u = 0; u < UB; ++u) {
-          const int64_t vi = v + (int64_t)u * kBT;
-          if (vi < v1) x[u] = ld_b<0>(vin + vi, pol_drop);
-        }
+          for (int u = 0; u < UB; ++u) {
+            const int64_t vi = v + (int64_t)u * kBT;
+            if (vi < v1) x[u] = ld_b<0>(vin + vi, pol_drop);
+          }
 #pragma unroll
-        for (int u = 0; u < UB; ++u) {
-          const int64_t vi = v + (int64_t)u * kBT;
-          if (vi < v1) {
-            float y[4] = {x[u].x * cf, x[u].y * cf, x[u].z * cf, x[u].w * cf};
-            put_vec<__nv_bfloat16, 4, float>(out + sg.head + vi * N, y);
+          for (int u = 0; u < UB; ++u) {
+            const int64_t vi = v + (int64_t)u * kBT;
+            if (vi < v1) {
+              float y[4] = {x[u].x * cf, x[u].y * cf, x[u].z * cf, x[u].w * cf};
+              put_vec<__nv_bfloat16, 4, float>(out + sg.head + vi * N, y);
+            }
           }
         }
-      }
-      const int64_t tail0 = sg.head + sg.nv * N;
-      if (c == 0 && gt < sg.head) out[gt] = __float2bfloat16_rn(in[gt] * cf);
-      if (c == G - 1 && gt < sg.n - tail0) out[tail0 + gt] = __float2bfloat16_rn(in[tail0 + gt] * cf);
-      group_sync<kBT>(kBarB);
-      if (gt == 0) {
-        // local stage writes -> gpu-scope release; the last CTA's system-scope
-        // release to the peers is cumulative over the whole chain
-        __threadfence();
-        if (atomicAdd(&f.pcount[s], 1u) == (unsigned)G - 1) {
-          __threadfence_system();
-          for (int q = 0; q < f.nranks; ++q) st_release_sys(flag(f, q, 0, f.rank, s), epoch);
+        const int64_t tail0 = sg.head + sg.nv * N;
+        if (c == 0 && gt < sg.head) out[gt] = __float2bfloat16_rn(in[gt] * cf);
+        if (c == G - 1 && gt < sg.n - tail0) out[tail0 + gt] = __float2bfloat16_rn(in[tail0 + gt] * cf);
+        group_sync<kBT>(kBarB);
+        if (gt == 0) {
+          __threadfence();
+          // last clip CTA of the group: publish "bucket s staged" with a
+          // gpu-scope release of this rank's own ready flag only.  A
+          // system-scope fence here measured 30+ µs per bucket under NVLink
+          // load and sat on the clip's critical path (2.07 vs 0.56 ms for the
+          // clip at N=4); the comm CTAs' forwarder warps pay it instead.
+          if (atomicAdd(&f.pcount[s], 1u) == (unsigned)G - 1) st_release_gpu(flag(f, f.rank, 0, f.rank, s), epoch);
+          s_bdone = i + 1;
         }
-        s_bdone = i + 1;
       }
+      if (gt == 0) stamp(p, 1);
     }
-    if (gt == 0) stamp(p, 1);
-  } else if constexpr (FLAT) {
-    // ================= C (flat): this CTA's slices of all its buckets as ONE
-    // stream — no per-bucket barrier or ragged tail; a bucket's ready flags
-    // are acquired by the first thread that reaches it and cached in smem
-    const int gt = t - kAT - kBT;
-    const int NR = f.nranks;
+  } else {
+    // ============================ comm CTA: reduce this rank's slice of every
+    // bucket (its 1/NC share), as one continuous stream in bucket order
+    const int NC = s_nc, cidx = s_idx;
     __shared__ int64_t s_beg[kMaxSegs + 1], s_voff[kMaxSegs];
     __shared__ uint32_t s_rdy[kMaxSegs];
-    __shared__ int s_sid[kMaxSegs];
-    int nb = 0;
-    for (int s = gid; s < p.nseg; s += R) ++nb;
-    if (gt == 0) {
+    if (t == 0) {
       int64_t acc = 0;
-      for (int i = 0; i < nb; ++i) {
-        const int s = gid + i * R;
+      for (int s = 0; s < p.nseg; ++s) {
         const Seg sg = p.seg[s];
         const int64_t nv8 = sg.n / 8;
         const int64_t per_r = (nv8 + NR - 1) / NR;
         const int64_t r0 = min64((int64_t)f.rank * per_r, nv8), r1 = min64(r0 + per_r, nv8);
-        const int64_t per_c = (r1 - r0 + G - 1) / G;
-        const int64_t c0 = min64(r0 + (int64_t)c * per_c, r1), c1 = min64(c0 + per_c, r1);
-        s_beg[i] = acc;
-        s_voff[i] = sg.out_off / 8 + c0 - acc;  // stage vector index = flat index + s_voff
-        s_sid[i] = s;
-        s_rdy[i] = 0u;
+        const int64_t per_c = (r1 - r0 + NC - 1) / NC;
+        const int64_t c0 = min64(r0 + (int64_t)cidx * per_c, r1), c1 = min64(c0 + per_c, r1);
+        s_beg[s] = acc;
+        s_voff[s] = sg.out_off / 8 + c0 - acc;
+        s_rdy[s] = 0u;
         acc += c1 - c0;
       }
-      s_beg[nb] = acc;
+      s_beg[p.nseg] = acc;
     }
-    group_sync<kCT>(kBarC);
-    const int64_t M = s_beg[nb];
+    __syncthreads();
+    const int64_t M = s_beg[p.nseg];
+    constexpr int kTC = kT - 32;  // the last warp forwards ready flags
+    if (t >= kTC) {
+      // forwarder: this rank's ready flag of bucket s (gpu-scope release by
+      // the clip) -> system fence -> every peer's flag area (sys release).
+      // Causality is transitive: clip stores -> gpu release/acquire -> sys
+      // release/acquire -> the peer's loads of this rank's stage.
+      if (t == kTC && NR > 1) {
+        for (int s = cidx; s < p.nseg; s += NC) {
+          wait_epoch(flag(f, f.rank, 0, f.rank, s), epoch);
+          __threadfence_system();
+          for (int q = 0; q < NR; ++q)
+            if (q != f.rank) st_release_sys(flag(f, q, 0, f.rank, s), epoch);
+        }
+      }
+    } else {
     int cur = 0;
-    for (int64_t f0 = gt; f0 < M; f0 += (int64_t)kCT * UC) {
+    for (int64_t f0 = t; f0 < M; f0 += (int64_t)kTC * UC) {
       uint4 x[UC][RMAX];
       int64_t vix[UC];
 #pragma unroll
       for (int u = 0; u < UC; ++u) {
-        const int64_t fi = f0 + (int64_t)u * kCT;
+        const int64_t fi = f0 + (int64_t)u * kTC;
         vix[u] = -1;
         if (fi < M) {
-          while (fi >= s_beg[cur + 1]) {
-            ++cur;
-            if (THR > 0 && gt == 0) s_cprog = cur;
-          }
+          while (fi >= s_beg[cur + 1]) ++cur;
           if (ld_acquire_cta_shared(&s_rdy[cur]) == 0u) {
-            for (int q = 0; q < NR; ++q) wait_epoch(flag(f, f.rank, 0, q, s_sid[cur]), epoch);
+            for (int q = 0; q < NR; ++q) wait_epoch(flag(f, f.rank, 0, q, cur), epoch);
             st_release_cta_shared(&s_rdy[cur], 1u);
-            if (cur == 0 && gt == 0) stamp(p, 2);
+            if (cur == 0 && t == 0) stamp(p, 2);
           }
           vix[u] = fi + s_voff[cur];
           if constexpr (MC) {
-            // NVSwitch sums the N stages (fp32 accumulate; the stages hold clip/N)
             asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
                          : "=r"(x[u][0].x), "=r"(x[u][0].y), "=r"(x[u][0].z), "=r"(x[u][0].w)
                          : "l"(reinterpret_cast<const uint4*>(f.mc) + vix[u])
@@ -319,26 +352,20 @@ __global__ void __launch_bounds__(kAT + kBT + kCT, 2) k_clip_allreduce_p2p(const
           } else {
 #pragma unroll
             for (int q = 0; q < RMAX; ++q)
-              if (q < NR) {
-                const uint4* src = reinterpret_cast<const uint4*>(f.stage[q]) + vix[u];
-                x[u][q] = CV ? __ldcv(src) : __ldcg(src);
-              }
+              if (q < NR) x[u][q] = __ldcg(reinterpret_cast<const uint4*>(f.stage[q]) + vix[u]);
           }
         }
       }
-      if constexpr (MC) {
-#pragma unroll
-        for (int u = 0; u < UC; ++u)
-          if (vix[u] >= 0)  // one store, multicast to every rank's stage
-            asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(
-                             reinterpret_cast<uint4*>(f.mc) + vix[u]),
-                         "f"(__uint_as_float(x[u][0].x)), "f"(__uint_as_float(x[u][0].y)),
-                         "f"(__uint_as_float(x[u][0].z)), "f"(__uint_as_float(x[u][0].w))
-                         : "memory");
-      } else {
 #pragma unroll
       for (int u = 0; u < UC; ++u) {
-        if (vix[u] >= 0) {
+        if (vix[u] < 0) continue;
+        if constexpr (MC) {
+          asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(
+                           reinterpret_cast<uint4*>(f.mc) + vix[u]),
+                       "f"(__uint_as_float(x[u][0].x)), "f"(__uint_as_float(x[u][0].y)),
+                       "f"(__uint_as_float(x[u][0].z)), "f"(__uint_as_float(x[u][0].w))
+                       : "memory");
+        } else {
           float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
           for (int q = 0; q < RMAX; ++q) {
@@ -357,110 +384,17 @@ __global__ void __launch_bounds__(kAT + kBT + kCT, 2) k_clip_allreduce_p2p(const
             if (q < NR) __stcg(reinterpret_cast<uint4*>(f.stage[q]) + vix[u], y);
         }
       }
-      }  // P2P
     }
-    if (THR > 0 && gt == 0) s_cprog = nb;
-    group_sync<kCT>(kBarC);
-    if (gt == 0) stamp(p, 3);
-    if (gt == 0) {
-      __threadfence_system();
-      if (atomicAdd(&f.pcount[kMaxSegs], 1u) == gridDim.x - 1) {
+    }  // reduce threads
+    __syncthreads();
+    if (t == 0) {
+      stamp(p, 3);
+      __threadfence_system();  // one system-scope release per CTA for all its remote stores
+      if (atomicAdd(&f.pcount[kMaxSegs], 1u) == (unsigned)NC - 1) {
         __threadfence_system();
         for (int q = 0; q < NR; ++q) st_release_sys(flag(f, q, 1, f.rank, 0), epoch);
       }
-      if (blockIdx.x == 0)
-        for (int q = 0; q < NR; ++q) wait_epoch(flag(f, f.rank, 1, q, 0), epoch);
-    }
-  } else {
-    // ================= C: two-shot allreduce of bucket s over NVLink
-    const int gt = t - kAT - kBT;
-    const int NR = f.nranks;
-    for (int s = gid; s < p.nseg; s += R) {
-      if (gt == 0)
-        for (int q = 0; q < NR; ++q) wait_epoch(flag(f, f.rank, 0, q, s), epoch);
-      group_sync<kCT>(kBarC);
-      const Seg sg = p.seg[s];
-      const int64_t nv8 = sg.n / 8;                   // 16 B = 8 bf16 (host guarantees n % 8 == 0)
-      const int64_t per_r = (nv8 + NR - 1) / NR;
-      const int64_t r0 = min64((int64_t)f.rank * per_r, nv8), r1 = min64(r0 + per_r, nv8);
-      const int64_t per_c = (r1 - r0 + G - 1) / G;
-      const int64_t c0 = min64(r0 + (int64_t)c * per_c, r1), c1 = min64(c0 + per_c, r1);
-      if constexpr (MC) {
-        // NVSwitch reduction: one multimem load-reduce (fp32 accumulate) and one
-        // multimem store (broadcast to every rank) per 16 B
-        const char* mcb = reinterpret_cast<const char*>(f.mc + sg.out_off);
-        for (int64_t v = c0 + gt; v < c1; v += (int64_t)kCT * UC) {
-          uint32_t r[UC][4];
-#pragma unroll
-          for (int u = 0; u < UC; ++u) {
-            const int64_t vi = v + (int64_t)u * kCT;
-            if (vi < c1)
-              asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
-                           : "=r"(r[u][0]), "=r"(r[u][1]), "=r"(r[u][2]), "=r"(r[u][3])
-                           : "l"(mcb + vi * 16)
-                           : "memory");
-          }
-#pragma unroll
-          for (int u = 0; u < UC; ++u) {
-            const int64_t vi = v + (int64_t)u * kCT;
-            if (vi < c1)
-              asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mcb + vi * 16),
-                           "f"(__uint_as_float(r[u][0])), "f"(__uint_as_float(r[u][1])),
-                           "f"(__uint_as_float(r[u][2])), "f"(__uint_as_float(r[u][3]))
-                           : "memory");
-          }
-        }
-      } else {
-      for (int64_t v = c0 + gt; v < c1; v += (int64_t)kCT * UC) {
-        uint4 x[UC][RMAX];
-#pragma unroll
-        for (int u = 0; u < UC; ++u) {
-          const int64_t vi = v + (int64_t)u * kCT;
-          if (vi < c1) {
-#pragma unroll
-            for (int q = 0; q < RMAX; ++q)
-              if (q < NR) {
-                const uint4* src = reinterpret_cast<const uint4*>(f.stage[q] + sg.out_off) + vi;
-                x[u][q] = CV ? __ldcv(src) : __ldcg(src);
-              }
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < UC; ++u) {
-          const int64_t vi = v + (int64_t)u * kCT;
-          if (vi < c1) {
-            float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-            for (int q = 0; q < RMAX; ++q) {
-              if (q < NR) {  // fixed rank order: identical bits on every rank
-                float e[8];
-                bf16x8_to_f32(x[u][q], e);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) acc[i] += e[i];
-              }
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) acc[i] *= f.inv_n;  // mean, not sum (gradsync.py:128)
-            const uint4 y = f32_to_bf16x8(acc);
-#pragma unroll
-            for (int q = 0; q < RMAX; ++q)
-              if (q < NR) __stcg(reinterpret_cast<uint4*>(f.stage[q] + sg.out_off) + vi, y);
-          }
-        }
-      }
-      }  // P2P two-shot
-    }
-    // one system-scope release per CTA for all of its remote stores, one
-    // done flag per rank; the launch completes only once every rank's slices
-    // of every bucket have landed here
-    group_sync<kCT>(kBarC);
-    if (gt == 0) {
-      __threadfence_system();
-      if (atomicAdd(&f.pcount[kMaxSegs], 1u) == gridDim.x - 1) {
-        __threadfence_system();
-        for (int q = 0; q < NR; ++q) st_release_sys(flag(f, q, 1, f.rank, 0), epoch);
-      }
-      if (blockIdx.x == 0)
+      if (cidx == 0)
         for (int q = 0; q < NR; ++q) wait_epoch(flag(f, f.rank, 1, q, 0), epoch);
     }
   }
@@ -474,40 +408,40 @@ __global__ void __launch_bounds__(kAT + kBT + kCT, 2) k_clip_allreduce_p2p(const
         f.pcount[s] = 0u;
       }
       f.pcount[kMaxSegs] = 0u;
+      reg[0] = reg[1] = reg[2] = 0u;
       p.counters[kMaxSegs] = 0u;
-      *f.epoch = epoch;  // every CTA read it at entry; the next launch sees epoch + 1
+      *f.epoch = epoch;
       __threadfence();
     }
   }
 }
 
-template <int AT, int BT, int CT, int UA, int UB, int UC, int RMAX, int CV, bool MC = false, bool FLAT = false,
-          int THR = 0>
-int launch_p2p(FusedParams& f, cudaStream_t stream) {
-  constexpr int kAT = AT, kBT = BT, kCT = CT;
-  auto kern = k_clip_allreduce_p2p<AT, BT, CT, UA, UB, UC, RMAX, CV, MC, FLAT, THR>;
+template <int AT, int BT, int UA, int UB, int UC, int RMAX, bool MC = false>
+int launch_split(FusedParams& f, cudaStream_t stream, int comm_sms) {
+  auto kern = k_clip_allreduce_split<AT, BT, UA, UB, UC, RMAX, MC>;
   const DeviceInfo& di = device_info();
   B2_REQUIRE(di.coop, B2_ERR_CUDA, "device does not support cooperative launch");
   static int occ_cached[64] = {};
   int& occ = occ_cached[di.device & 63];
   if (occ == 0) {
-    B2_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kAT + kBT + kCT, 0));
+    B2_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, AT + BT, 0));
     B2_REQUIRE(occ >= 1, B2_ERR_CUDA, "fused kernel cannot be resident");
   }
-  const int grid = std::min(di.sm_count * std::min(2, occ), kMaxGrid);
-  f.p.ngroups = choose_groups(f.p, grid, sizeof(float));
-  for (int s = 0; s < f.p.nseg; ++s) {
-    Seg& sg = f.p.seg[s];
-    const int gs = group_size(grid, f.p.ngroups, s % f.p.ngroups);
-    sg.nv = (sg.n - sg.head) / 4;
-    sg.per = (sg.nv + gs - 1) / gs;
-  }
+  const int per_sm = std::min(2, occ);
+  const int grid = std::min(di.sm_count * per_sm, kMaxGrid);
+  comm_sms = std::max(1, std::min(comm_sms, di.sm_count - 1));
+  f.comm_sms = comm_sms;
+  // groups are sized for the clip CTAs the placement will give (one per
+  // resident slot on the clip SMs); the device re-derives chunks from the
+  // actual registration counts
+  f.p.ngroups = choose_groups(f.p, grid - comm_sms * per_sm, sizeof(float));
+  for (int s = 0; s < f.p.nseg; ++s) f.p.seg[s].nv = (f.p.seg[s].n - f.p.seg[s].head) / 4;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kAT + kBT + kCT);
+  cfg.blockDim = dim3(AT + BT);
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;  // CTAs wait on each other's partials
+  attr[0].id = cudaLaunchAttributeCooperative;  // registration barrier + cross-CTA waits
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
@@ -617,54 +551,19 @@ static int clip_allreduce_impl(const void* in, void* const* stages, void* mc_sta
   f.inv_n = 1.0f / (float)nranks;
   f.mc = static_cast<__nv_bfloat16*>(mc_stage);
 
-  // the reduce group keeps UC x RMAX 16 B vectors in flight: 32 registers
+  // roles: comm CTAs on the first `cs` SMs (B2_COMM_SMS overrides), clip CTAs
+  // on the rest.  Sweeps (profiles/r01_k4_split_sweep.jsonl): P2P best at 64
+  // of 148 SMs for N = 2 and 4, NVLS at 32.
   cudaStream_t st = (cudaStream_t)stream;
-  static int cfg = -1;  // tuning knob: B2_FUSED_CFG selects the warp-group split (A/B/C threads)
-  if (cfg < 0) {
-    const char* e = getenv("B2_FUSED_CFG");
-    cfg = e ? atoi(e) : 0;
+  static int csms = -1;
+  if (csms < 0) {
+    const char* e = getenv("B2_COMM_SMS");
+    csms = e ? atoi(e) : 0;
   }
-  if (mc_stage) {  // RMAX 1: one multimem load per vector
-    switch (cfg) {
-      case 1: return launch_p2p<256, 128, 128, 8, 4, 4, 1, 1, true>(f, st);
-      case 2: return launch_p2p<128, 256, 128, 8, 4, 8, 1, 1, true, true>(f, st);
-      case 3: return launch_p2p<128, 256, 128, 8, 4, 16, 1, 1, true, true>(f, st);
-      default: return launch_p2p<128, 256, 128, 8, 4, 8, 1, 1, true, true>(f, st);
-    }
-  }
-  if (nranks <= 2) {
-    switch (cfg) {
-      case 1: return launch_p2p<128, 128, 256, 8, 4, 4, 2, 1>(f, st);
-      case 2: return launch_p2p<256, 128, 128, 8, 4, 4, 2, 0>(f, st);
-      case 5: return launch_p2p<192, 192, 128, 8, 4, 4, 2, 1>(f, st);
-      case 6: return launch_p2p<160, 224, 128, 8, 4, 4, 2, 1>(f, st);
-      case 7: return launch_p2p<192, 160, 160, 8, 4, 4, 2, 1>(f, st);
-      case 10: return launch_p2p<256, 128, 128, 8, 4, 4, 2, 1, false, true>(f, st);
-      case 11: return launch_p2p<256, 128, 128, 8, 4, 8, 2, 1, false, true>(f, st);
-      case 12: return launch_p2p<256, 128, 128, 8, 4, 4, 2, 0, false, true>(f, st);
-      case 13: return launch_p2p<192, 160, 160, 8, 4, 4, 2, 1, false, true>(f, st);
-      case 18: return launch_p2p<192, 192, 128, 8, 4, 8, 2, 1, false, true>(f, st);
-      case 19: return launch_p2p<128, 256, 128, 8, 4, 8, 2, 1, false, true>(f, st);
-      case 20: return launch_p2p<256, 128, 128, 8, 8, 8, 2, 1, false, true>(f, st);
-      case 21: return launch_p2p<192, 192, 128, 8, 8, 8, 2, 1, false, true>(f, st);
-      case 22: return launch_p2p<160, 224, 128, 8, 4, 8, 2, 1, false, true>(f, st);
-      case 9: return launch_p2p<256, 128, 128, 8, 4, 4, 2, 1>(f, st);  // per-bucket C (round-1 v1)
-      default: return launch_p2p<128, 256, 128, 8, 4, 8, 2, 1, false, true>(f, st);
-    }
-  }
-  if (nranks <= 4) {
-    switch (cfg) {
-      case 5: return launch_p2p<192, 192, 128, 8, 4, 2, 4, 1>(f, st);
-      case 6: return launch_p2p<160, 224, 128, 8, 4, 2, 4, 1>(f, st);
-      case 7: return launch_p2p<192, 160, 160, 8, 4, 2, 4, 1>(f, st);
-      case 10: return launch_p2p<256, 128, 128, 8, 4, 2, 4, 1, false, true>(f, st);
-      case 11: return launch_p2p<256, 128, 128, 8, 4, 4, 4, 1, false, true>(f, st);
-      case 12: return launch_p2p<128, 256, 128, 8, 4, 4, 4, 1, false, true>(f, st);
-      case 13: return launch_p2p<192, 192, 128, 8, 4, 4, 4, 1, false, true>(f, st);
-      case 14: return launch_p2p<128, 256, 128, 8, 4, 2, 4, 1, false, true>(f, st);
-      case 9: return launch_p2p<256, 128, 128, 8, 4, 2, 4, 1>(f, st);  // per-bucket C (round-1 v1)
-      default: return launch_p2p<128, 256, 128, 8, 4, 4, 4, 1, false, true>(f, st);
-    }
-  }
-  return launch_p2p<128, 256, 128, 8, 4, 2, 8, 1, false, true>(f, st);
+  const int cs = csms > 0 ? csms : (mc_stage ? 32 : 64);
+  // each reduce thread keeps UC x RMAX 16 B vectors in flight (32 registers)
+  if (mc_stage) return launch_split<192, 320, 8, 4, 8, 1, true>(f, st, cs);
+  if (nranks <= 2) return launch_split<192, 320, 8, 4, 4, 2>(f, st, cs);
+  if (nranks <= 4) return launch_split<192, 320, 8, 4, 2, 4>(f, st, cs);
+  return launch_split<192, 320, 8, 4, 1, 8>(f, st, cs);
 }

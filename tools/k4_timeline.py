@@ -29,6 +29,7 @@ NAMES = ["start", "clip_done", "c_first_ready", "reduce_done", "exit"]
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--mb", type=int, default=25)
+    ap.add_argument("--transport", default="p2p", choices=("p2p", "nvls"))
     args = ap.parse_args()
     if "LOCAL_RANK" not in os.environ:  # single process (e.g. under ncu): a world of one
         os.environ.update(RANK="0", LOCAL_RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1", MASTER_PORT="29791")
@@ -43,7 +44,7 @@ def main():
     dim = synthetic.BERT_LARGE_DIM
     g, _, _ = synthetic.bert_grads(dim, rank=rank)
     layout = B.capped_bucket_layout(dim, args.mb * 1024 * 1024 // 4)
-    sync = FusedBucketSync(layout, B.ClipConfig(1.0, "bucket_wise"), transport="p2p")
+    sync = FusedBucketSync(layout, B.ClipConfig(1.0, "bucket_wise"), transport=args.transport)
     for _ in range(5):
         sync.sync(g)
     torch.cuda.synchronize()
@@ -54,10 +55,12 @@ def main():
     raw = ws[: K_MAX_SEGS * K_MAX_GRID * 8].view(torch.int64).view(K_MAX_SEGS, K_MAX_GRID).cpu().numpy()
     grid = torch.cuda.get_device_properties(0).multi_processor_count * 2
     st = np.stack([raw[K_MAX_SEGS - 1 - k, :grid] for k in range(5)]).astype(np.float64)
-    t0 = st[0].min()
-    out = {"rank": rank, "cfg": os.environ.get("B2_FUSED_CFG", "0"), "bucket_mb": args.mb, "buckets": len(layout)}
+    t0 = st[0][st[0] > 0].min()
+    out = {"rank": rank, "transport": args.transport, "cfg": os.environ.get("B2_FUSED_CFG", "0"), "bucket_mb": args.mb, "buckets": len(layout)}
     for k, n in enumerate(NAMES):
-        v = (st[k] - t0) / 1e3
+        v = (st[k][st[k] > 0] - t0) / 1e3  # roles stamp only their own events
+        if v.size == 0:
+            continue
         out[n] = [round(float(v.min()), 1), round(float(np.median(v)), 1), round(float(v.max()), 1)]
     allo = [None] * dist.get_world_size()
     dist.all_gather_object(allo, out)

@@ -14,6 +14,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <vector>
+#include <cstdlib>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); exit(1); } } while (0)
 
@@ -77,6 +78,77 @@ __global__ void k_twoshot(uint4* __restrict__ local, uint4* __restrict__ peer, i
       }
     }
   }
+}
+
+// LDGSTS pull: per thread a ring of D 16 B async copies from the peer into smem
+template <int D>
+__global__ void k_pull_ldgsts(const uint4* __restrict__ peer, int64_t nv, uint32_t* sink) {
+  extern __shared__ uint4 ring[];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  uint32_t a = 0;
+  auto slot = [&](int d) { return (uint32_t)__cvta_generic_to_shared(&ring[d * blockDim.x + threadIdx.x]); };
+  for (int d = 0; d < D - 1; ++d) {
+    const int64_t j = i0 + d * stride;
+    if (j < nv) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(slot(d)), "l"(peer + j) : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  for (int64_t k = 0;; ++k) {
+    const int64_t j = i0 + k * stride;
+    if (j >= nv) break;
+    const int64_t jn = i0 + (k + D - 1) * stride;
+    if (jn < nv)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(slot((int)((k + D - 1) % D))), "l"(peer + jn) : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");
+    const uint4 v = ring[(k % D) * blockDim.x + threadIdx.x];
+    a ^= v.x ^ v.w;
+  }
+  if (a == 0x12345678u) sink[threadIdx.x] = a;
+}
+
+// TMA bulk pull: one elected thread streams CH-byte pieces of the CTA's
+// contiguous share of the peer buffer into an NS-slot smem ring (mbarriers)
+template <int CH, int NS>
+__global__ void k_pull_tma(const char* __restrict__ peer, int64_t bytes, uint32_t* sink) {
+  extern __shared__ __align__(128) char tring[];
+  __shared__ __align__(8) uint64_t full[NS];
+  const int64_t per = (bytes / gridDim.x) & ~(int64_t)(CH - 1);
+  const char* src = peer + blockIdx.x * per;
+  const int npieces = (int)(per / CH);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&full[i])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t a = 0;
+  if (threadIdx.x == 0) {
+    auto issue = [&](int piece) {
+      const int sl = piece % NS;
+      const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&full[sl]);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(CH) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(tring + sl * CH)),
+                   "l"(src + (int64_t)piece * CH), "r"(CH), "r"(bar)
+                   : "memory");
+    };
+    for (int p = 0; p < NS && p < npieces; ++p) issue(p);
+    for (int p = 0; p < npieces; ++p) {
+      const int sl = p % NS;
+      const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&full[sl]);
+      const uint32_t phase = (p / NS) & 1;
+      uint32_t done = 0;
+      while (!done)
+        asm volatile("{ .reg .pred P; mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2; selp.u32 %0, 1, 0, P; }"
+                     : "=r"(done)
+                     : "r"(bar), "r"(phase)
+                     : "memory");
+      a ^= *reinterpret_cast<const uint32_t*>(tring + sl * CH);
+      if (p + NS < npieces) issue(p + NS);
+    }
+  }
+  if (a == 0x12345678u) sink[threadIdx.x] = a;
 }
 
 struct Dev {
@@ -152,6 +224,18 @@ int main() {
     SWEEP("pull", both, (double)S, (k_pull<U><<<grid, t, 0, d[g].st>>>(d[1 - g].buf, nv, d[g].sink)))
     SWEEP("push", both, (double)S, (k_push<U><<<grid, t, 0, d[g].st>>>(d[1 - g].buf, nv)))
   }
+  for (int both = 0; both < 2; ++both) {
+    for (int t : {128, 256}) {
+      {constexpr int D = 8; const size_t sm = (size_t)D * t * 16; float ms = run(d, iters, [&](int g) { if (both || g == 0) { cudaFuncSetAttribute(k_pull_ldgsts<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000); k_pull_ldgsts<D><<<296, t, sm, d[g].st>>>(d[1 - g].buf, nv, d[g].sink);} }); report("pull_ldgsts_d8", both, 2, t, D, ms, (double)S);}
+      {constexpr int D = 16; const size_t sm = (size_t)D * t * 16; float ms = run(d, iters, [&](int g) { if (both || g == 0) { cudaFuncSetAttribute(k_pull_ldgsts<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000); k_pull_ldgsts<D><<<296, t, sm, d[g].st>>>(d[1 - g].buf, nv, d[g].sink);} }); report("pull_ldgsts_d16", both, 2, t, D, ms, (double)S);}
+    }
+    for (int bps : {1, 2}) {
+      {constexpr int CH = 4096, NS = 8; float ms = run(d, iters, [&](int g) { if (both || g == 0) { cudaFuncSetAttribute(k_pull_tma<CH, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000); k_pull_tma<CH, NS><<<148 * bps, 32, CH * NS, d[g].st>>>((const char*)d[1 - g].buf, S, d[g].sink);} }); report("pull_tma_4k_x8", both, bps, 32, 0, ms, (double)S);}
+      {constexpr int CH = 16384, NS = 4; float ms = run(d, iters, [&](int g) { if (both || g == 0) { cudaFuncSetAttribute(k_pull_tma<CH, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000); k_pull_tma<CH, NS><<<148 * bps, 32, CH * NS, d[g].st>>>((const char*)d[1 - g].buf, S, d[g].sink);} }); report("pull_tma_16k_x4", both, bps, 32, 0, ms, (double)S);}
+      {constexpr int CH = 8192, NS = 8; float ms = run(d, iters, [&](int g) { if (both || g == 0) { cudaFuncSetAttribute(k_pull_tma<CH, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000); k_pull_tma<CH, NS><<<148 * bps, 32, CH * NS, d[g].st>>>((const char*)d[1 - g].buf, S, d[g].sink);} }); report("pull_tma_8k_x8", both, bps, 32, 0, ms, (double)S);}
+    }
+  }
+  if (getenv("MB_ONLY_ASYNC")) return 0;
   // two-shot: GPU g reduces slice g of the (2 x S) buffer: local slice + the peer's same slice
   SWEEP("2shot", 1, (double)S,
         (k_twoshot<U><<<grid, t, 0, d[g].st>>>(d[g].buf + g * nv, d[1 - g].buf + g * nv, nv)))
