@@ -511,7 +511,121 @@ def bench_presort(args):
             "k3_presort_deal": {"ms": t3, "achieved_gbs": k3_gbs, "frac": k3_gbs / hbm, "bytes_per_key": 12,
                                 "launches": 1},
         }
+    # a 10x batched run (100 M keys) shows the asymptote once
+    # launch latency no longer matters: the corpus tiled 10x through K2 (8
+    # shards of 12.5 M) and the lb-16 epoch's pools tiled 10x through K3
+    reps = 10
+    big_lens = d_lens.repeat(reps)
+    nbig = big_lens.numel()
+    ws_big = lib.b2_strata_workspace_bytes(nbig)
+    wsb = torch.empty(ws_big, dtype=torch.uint8, device="cuda")
+    ids_big = torch.empty(nbig, dtype=torch.int32, device="cuda")
+    offs_big = _lib.i64_array(r * (nbig // SHARDS) for r in range(SHARDS + 1))
+    ids16, ln16, steps16 = pools[16]
+    b_ids = torch.from_numpy(ids16).cuda().repeat(reps)
+    b_ln = torch.from_numpy(ln16).cuda().repeat(reps)
+    b_out = torch.empty_like(b_ids)
+    b_tok = torch.empty((steps16 * reps, GPN), dtype=torch.int64, device="cuda")
+    pbad = torch.empty(1, dtype=torch.int64, device="cuda")
+
+    def k2b():
+        _lib.check(lib.b2_strata_partition_shards(
+            big_lens.data_ptr(), None, offs_big, SHARDS, bnds, 4, ids_big.data_ptr(), counts.data_ptr(),
+            bad.data_ptr(), wsb.data_ptr(), ws_big, sp))
+
+    def k3b():
+        _lib.check(lib.b2_presort_deal(b_ids.data_ptr(), b_ln.data_ptr(), steps16 * reps, GPN * 16, GPN, 1, 512,
+                                       CORPUS_N - 1, b_out.data_ptr(), None, b_tok.data_ptr(), pbad.data_ptr(), sp))
+
+    for _ in range(2):
+        k2b(); k3b()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    t2 = t3 = 0.0
+    nrep = max(3, min(args.steps, 10))
+    for _ in range(nrep):
+        torch.cuda.synchronize()
+        ev[0].record(); k2b(); ev[1].record(); k3b(); ev[2].record()
+        torch.cuda.synchronize()
+        t2 += ev[0].elapsed_time(ev[1]) / nrep
+        t3 += ev[1].elapsed_time(ev[2]) / nrep
+    hbm = peaks()["hbm_gbs"]
+    res["batched_10x_lb16"] = {
+        "keys": int(nbig), "keys_per_s": nbig / ((t2 + t3) * 1e-3), "ms": t2 + t3,
+        "k2_partition": {"ms": t2, "achieved_gbs": nbig * 8 / (t2 * 1e-3) / 1e9,
+                         "frac": nbig * 8 / (t2 * 1e-3) / 1e9 / hbm},
+        "k3_presort_deal": {"ms": t3, "achieved_gbs": b_ids.numel() * 12 / (t3 * 1e-3) / 1e9,
+                            "frac": b_ids.numel() * 12 / (t3 * 1e-3) / 1e9 / hbm},
+        "note": "corpus and epoch pools tiled 10x (inputs 0.4-1.2 GB >> L2)"}
     return res
+
+
+def bench_mcsim(args, lens):
+    """the Monte-Carlo balance engine at paper scale
+    (Topology(128, 8) = 1,024 GPUs, lb 16, LOCAL_PRESORT + snake, the 10 M corpus).
+    Unit: keys = trials x lb x GPUs drawn, dealt and summed."""
+    import torch
+
+    from paper_2402_02447_b200 import Topology
+    from paper_2402_02447_b200.mcsim import BalanceExperiment, _prepare, draw_trials, run_trials, trial_token_counts
+
+    T = args.mc_trials
+    exp = BalanceExperiment("local_presort", Topology(128, 8), lens, seed=CORPUS_SEED, local_batch=16, trials=T,
+                            scan="snake")
+    prep = _prepare(exp)
+    keys_per_trial = 16 * 1024
+    threads = len(os.sched_getaffinity(0))
+    # draws alone (host threads)
+    n_d = min(T, 4096)
+    t0 = time.perf_counter()
+    mat = draw_trials(exp, 0, n_d, prep=prep, threads=threads)
+    t_draw = time.perf_counter() - t0
+    # kernel alone (device-resident matrices, CUDA events)
+    dmat = torch.from_numpy(mat).cuda()
+    for _ in range(3):
+        trial_token_counts(exp, dmat, prep.max_len)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    torch.cuda.synchronize()
+    ev[0].record()
+    for _ in range(10):
+        trial_token_counts(exp, dmat, prep.max_len)
+    ev[1].record()
+    torch.cuda.synchronize()
+    t_k = ev[0].elapsed_time(ev[1]) / 10 * 1e-3
+    # end to end (draws overlapped with H2D + kernel, then the reference's aggregation)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    mins, maxs = run_trials(exp, chunk=4096, threads=threads)
+    t_e2e = time.perf_counter() - t0
+    kbytes = n_d * keys_per_trial * 4  # int32 length read per key
+    return {"metric": "mc keys/s", "unit": "keys/s",
+            "config": f"BalanceExperiment(LOCAL_PRESORT, snake, Topology(128, 8), lb 16, {T} trials, 10M corpus)",
+            "keys": T * keys_per_trial, "keys_per_s": T * keys_per_trial / t_e2e, "seconds": t_e2e,
+            "avg_min": float(mins.mean()), "avg_max": float(maxs.mean()),
+            "draws": {"keys_per_s": n_d * keys_per_trial / t_draw, "threads": threads,
+                      "impl": "b2_mc_draw (bit-exact numpy SeedSequence/PCG64/choice port, host C++)"},
+            "kernel": {"keys_per_s": n_d * keys_per_trial / t_k, "ms_per_4096_trials": t_k * 1e3,
+                       "achieved_gbs": kbytes / t_k / 1e9, "frac": kbytes / t_k / 1e9 / peaks()["hbm_gbs"],
+                       "bytes_per_key": 4}}
+
+
+def cpu_mcsim_baseline(lens: np.ndarray, trials: int = 40) -> dict:
+    """The reference algorithm on the host (oracle numpy, strata prepared once
+    like mcsim._prepare): per-trial draws + local presort + min/max."""
+    from oracle import ddp_oracle as O
+
+    pools, probs = O.stratify(lens, BOUNDS, ids=np.arange(lens.size))
+    counts = O.allocate_counts(probs, 16)
+    pl = [lens[np.asarray(p, dtype=np.int64)] for p in pools]
+    G = 1024
+    t0 = time.perf_counter()
+    for t in range(trials):
+        rng = np.random.default_rng(np.random.SeedSequence(entropy=CORPUS_SEED, spawn_key=(t,)))
+        blocks = [p[rng.choice(p.size, size=c * G, replace=False)].reshape(c, G) for c, p in zip(counts, pl) if c]
+        tok = O.mcsim_local_presort_tokens(np.concatenate(blocks), 128, 8, True)
+        tok.min(), tok.max()
+    dt = time.perf_counter() - t0
+    return {"value": trials * 16 * G / dt, "unit": "keys/s", "cores": 1, "kind": "port",
+            "sample": f"{trials} trials of the 1,024-GPU LOCAL_PRESORT experiment (oracle numpy loop, strata prepared once)"}
 
 
 # --------------------------------------------------------------------- CPU baselines
@@ -610,6 +724,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-presort", action="store_true")
     ap.add_argument("--no-bert", action="store_true")
+    ap.add_argument("--no-mcsim", action="store_true")
+    ap.add_argument("--mc-trials", type=int, default=20000)
     ap.add_argument("--comm", choices=("fused", "nccl"), default="fused",
                     help="N>1: fused clip+NVLink allreduce kernel (default) or per-bucket NCCL")
     args = ap.parse_args()
@@ -642,6 +758,11 @@ def main():
     presort = None
     if rank == 0 and not args.no_presort:
         presort = bench_presort(args)
+    mc = None
+    if rank == 0 and not args.no_mcsim:
+        from paper_2402_02447_b200.seqdata import LengthDistribution, generate_lengths
+
+        mc = bench_mcsim(args, generate_lengths(LengthDistribution(), CORPUS_N, CORPUS_SEED))
     if rank == 0:
         line = {
             "metric": "clip+allreduce GB/s", "value": r["value"], "unit": "GB/s", "n_gpus": world,
@@ -663,11 +784,18 @@ def main():
             line["presort"] = {"metric": "presort keys/s", "unit": "keys/s",
                                "config": "10M lengths (seed 2402) over 8 shards, Topology(1,8), snake, whole epoch",
                                "l2": "flushed (512 MB write) before every timed iteration", **presort}
+        if mc is not None:
+            line["mcsim"] = mc
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_clip_baseline(sample, 52)
             if presort is not None:
                 lens, pools, _ = presort_inputs()
                 line["presort"]["cpu_baseline"] = cpu_presort_baseline(lens, pools)
+            if mc is not None:
+                from paper_2402_02447_b200.seqdata import LengthDistribution, generate_lengths
+
+                line["mcsim"]["cpu_baseline"] = cpu_mcsim_baseline(
+                    generate_lengths(LengthDistribution(), CORPUS_N, CORPUS_SEED))
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

@@ -219,6 +219,30 @@ int b2_presort_deal(const int32_t* ids, const int32_t* lens, int64_t nseg, int s
                     int lanes, int scan, int32_t max_len, int32_t max_id, int32_t* out_ids,
                     int32_t* out_pos, int64_t* tokens, int64_t* bad, void* stream);
 
+/* Monte-Carlo balance engine, host draws.
+ *
+ * Replaces the per-trial draws of mcsim (mcsim.py:146-151 _draw_uniform,
+ * :166-180 _stratified_matrix) under derive_rng(seed, t) (seeding.py:8-16),
+ * bit-exact with numpy 2.x.  lengths holds the strata's lengths concatenated
+ * (pool_sizes[k] each; one stratum = the whole corpus for NONE /
+ * GLOBAL_PRESORT).  Trial first_trial + i writes out[i][b*num_gpus], the
+ * (b, G) matrix row-major, b = sum(counts).  Host memory; nthreads host
+ * threads.  counts[k]*num_gpus > pool_sizes[k] -> B2_ERR_INVALID (the
+ * reference's "corpus exhausted within a trial"). */
+int b2_mc_draw(const int32_t* lengths, const int64_t* pool_sizes, int nstrata, const int64_t* counts,
+               int num_gpus, uint64_t seed, int64_t first_trial, int64_t ntrials, int nthreads, int32_t* out);
+
+/* Monte-Carlo balance engine, device side: per-trial per-GPU token counts
+ * and their min/max (mcsim._trial_token_counts :182-213, _run :284-300).
+ * strategy: 0 NONE, 1 STRATIFIED (column sums), 2 LOCAL_PRESORT (per-node
+ * pool sorted descending + deal; b*gpus_per_node <= 512), 3 GLOBAL_PRESORT.
+ * mat [ntrials][b*num_gpus] lengths in [1, max_len] (max_len <= 4096,
+ * num_gpus <= 2048); counts [ntrials][num_gpus] may be NULL; mins/maxs
+ * [ntrials] int64; *bad = 1 if a length was out of range.  Device memory. */
+int b2_mc_token_counts(const int32_t* mat, int64_t ntrials, int b, int num_gpus, int gpus_per_node, int strategy,
+                       int scan, int32_t max_len, int64_t* counts, int64_t* mins, int64_t* maxs, int32_t* bad,
+                       void* stream);
+
 #ifdef __cplusplus
 }
 #endif

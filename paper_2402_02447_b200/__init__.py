@@ -2,7 +2,7 @@
 
 H1 (bucket-wise clip before allreduce): ``gradsync`` + ``ddp`` (NCCL side
 stream, DDP comm hook).  H2 (stratified local presort): ``strata`` +
-``balance``.  All data passes run in ``_native/libb2ddp.so`` (sm_100a); see
+``balance``; the Monte-Carlo balance engine in ``mcsim``.  All data passes run in ``_native/libb2ddp.so`` (sm_100a); see
 DESIGN.md.  Names mirror ``ddpsim/__init__.py:14-103`` for the in-scope paths.
 """
 
@@ -45,6 +45,8 @@ from .strata import (
     derive_seed,
 )
 
+from .mcsim import BalanceExperiment, BalanceStats, Strategy, run_ablation, run_balance_experiment
+
 __version__ = "0.1.0"
 
 __all__ = [
@@ -56,4 +58,5 @@ __all__ = [
     "Sample", "Topology", "generate_corpus", "generate_lengths",
     "DeviceStrata", "Strata", "StratumAllocation", "allocate_counts", "draw_batch",
     "stratify", "stratify_lengths", "stratify_shards", "NativeDraws", "derive_seed",
+    "BalanceExperiment", "BalanceStats", "Strategy", "run_ablation", "run_balance_experiment",
 ]

@@ -9,12 +9,12 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
-SOURCES = ["capi.cu", "bucket_clip.cu", "fused_allreduce.cu", "comm.cu", "strata.cu", "presort.cu", "draws.cpp"]
+SOURCES = ["capi.cu", "bucket_clip.cu", "fused_allreduce.cu", "comm.cu", "strata.cu", "presort.cu", "mc.cu", "draws.cpp"]
 OUT = PKG / "_native" / "libb2ddp.so"
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared", "-ldl",
+    "-Xcompiler", "-fPIC", "-shared", "-ldl", "-lpthread",
 ]
 
 

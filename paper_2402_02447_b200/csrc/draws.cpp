@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <thread>
 #include <vector>
 
 #include "b2ddp.h"
@@ -96,8 +97,8 @@ struct Pcg64 {
   int has_u32 = 0;
   uint32_t u32 = 0;
   static constexpr u128 MULT = ((u128)0x2360ED051FC65DA4ull << 64) | 0x4385DF649FCCF645ull;
-  explicit Pcg64(uint64_t seed) {  // default_rng(seed)
-    SeedSeq ss(seed, nullptr, 0);
+  explicit Pcg64(uint64_t seed) : Pcg64(SeedSeq(seed, nullptr, 0)) {}  // default_rng(seed)
+  explicit Pcg64(const SeedSeq& ss) {  // default_rng(SeedSequence(...)): seeding.derive_rng
     uint64_t v[4];
     ss.generate_u64(v, 4);
     const u128 initstate = ((u128)v[0] << 64) | v[1];
@@ -332,5 +333,62 @@ extern "C" int b2_draw_epoch(b2_draw_state* st, const int64_t* counts, uint64_t 
     if (rc != B2_OK) return rc;
     *done = t + 1;
   }
+  return B2_OK;
+}
+
+// ---------------------------------------------------------------- Monte-Carlo trials
+// mcsim.py (the balance experiment's per-trial draws): trial t uses
+// derive_rng(seed, t) = default_rng(SeedSequence(seed, spawn_key=(t,)))
+// (seeding.py:8-16).  For each stratum k with counts[k] > 0, in order,
+// need = counts[k] * G lengths are drawn as lens_k[choice(|pool_k|, need,
+// replace=False)] and appended (_stratified_matrix, mcsim.py:166-180; the
+// uniform draw of NONE / GLOBAL_PRESORT, :146-151, is the one-stratum case).
+// out[t] is therefore the (b, G) length matrix, row-major.  Pools are not
+// mutated (unlike draw_batch).  Trials are independent: `nthreads` host
+// threads take contiguous trial ranges.
+extern "C" int b2_mc_draw(const int32_t* lengths, const int64_t* pool_sizes, int nstrata, const int64_t* counts,
+                          int num_gpus, uint64_t seed, int64_t first_trial, int64_t ntrials, int nthreads,
+                          int32_t* out) {
+  if (!lengths || !pool_sizes || !counts || !out || nstrata < 1 || num_gpus < 1 || ntrials < 0 || first_trial < 0) {
+    b2::set_error("b2_mc_draw: bad arguments");
+    return B2_ERR_INVALID;
+  }
+  std::vector<int64_t> off(nstrata + 1, 0);
+  int64_t per_trial = 0;
+  for (int k = 0; k < nstrata; ++k) {
+    off[k + 1] = off[k] + pool_sizes[k];
+    const int64_t need = counts[k] * (int64_t)num_gpus;
+    if (counts[k] < 0 || need > pool_sizes[k]) {
+      b2::set_error("corpus exhausted within a trial: a stratum holds %lld samples but the trial needs %lld",
+                    (long long)pool_sizes[k], (long long)need);
+      return B2_ERR_INVALID;
+    }
+    per_trial += need;
+  }
+  if (ntrials == 0) return B2_OK;
+  const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(nthreads > 0 ? nthreads : 1, ntrials));
+  auto work = [&](int64_t t0, int64_t t1) {
+    std::vector<int64_t> picked, scratch;
+    std::vector<uint64_t> set;
+    for (int64_t t = t0; t < t1; ++t) {
+      const uint64_t key = (uint64_t)(first_trial + t);
+      Pcg64 rng(SeedSeq(seed, &key, 1));
+      int32_t* o = out + t * per_trial;
+      for (int k = 0; k < nstrata; ++k) {
+        const int64_t need = counts[k] * (int64_t)num_gpus;
+        if (need == 0) continue;
+        rng.choice(pool_sizes[k], need, picked, scratch, set);
+        const int32_t* lk = lengths + off[k];
+        for (int64_t i = 0; i < need; ++i) *o++ = lk[picked[i]];
+      }
+    }
+  };
+  std::vector<std::thread> th;
+  const int64_t chunk = (ntrials + nt - 1) / nt;
+  for (int i = 0; i < nt; ++i) {
+    const int64_t t0 = i * chunk, t1 = std::min<int64_t>(ntrials, t0 + chunk);
+    if (t0 < t1) th.emplace_back(work, t0, t1);
+  }
+  for (auto& x : th) x.join();
   return B2_OK;
 }

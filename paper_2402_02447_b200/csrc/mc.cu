@@ -1,0 +1,211 @@
+// Monte-Carlo balance engine, device side: per-trial
+// per-GPU token counts and their min / max, for every trial in one launch.
+//
+// Reference: mcsim._trial_token_counts (mcsim.py:182-213) and _run
+// (:284-300).  Input: the (b, G) length matrix of each trial, row-major (the
+// host draws, b2_mc_draw).  Per strategy:
+//   NONE, STRATIFIED  column sums (:186-188, :198-199);
+//   LOCAL_PRESORT     per node: the pool (rows x that node's gpn columns, row
+//                     order) sorted descending by value, dealt back as (b, gpn)
+//                     rows, odd rows reversed under SNAKE, column sums
+//                     (:201-212, _snake_flip :160-163);
+//   GLOBAL_PRESORT    the same over all b*G values at once (:190-196).
+// Only values are sorted (np.sort), so ties need no tie-break.  Sums are
+// exact int64.  Layout: one CTA per trial (grid-stride), per-GPU counts in
+// shared memory; LOCAL pools of <= 512 values sort in one warp (bitonic,
+// registers); GLOBAL pools use a counting sort (lengths lie in [1, max_len])
+// whose descending positions are resolved by binary search.
+#include "bitonic.cuh"
+#include "common.cuh"
+
+#include <climits>
+
+namespace b2 {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kMaxGpus = 2048;   // per-CTA int64 counts in shared memory: 16 KB
+constexpr int kMaxLenBins = 4096;
+
+struct McParams {
+  const int32_t* mat;
+  int64_t ntrials;
+  int b, G, gpn, strategy, snake, max_len;
+  int64_t* counts;  // [ntrials][G] or null
+  int64_t* mins;
+  int64_t* maxs;
+  int* bad;         // set to 1 if a length is outside [1, max_len]
+};
+
+__device__ __forceinline__ void block_minmax(int64_t& mn, int64_t& mx, int64_t* s_mn, int64_t* s_mx) {
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = min(mn, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)mn, o));
+    mx = max(mx, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)mx, o));
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    s_mn[w] = mn;
+    s_mx[w] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < kThreads / 32; ++i) {
+      s_mn[0] = min(s_mn[0], s_mn[i]);
+      s_mx[0] = max(s_mx[0], s_mx[i]);
+    }
+  }
+  __syncthreads();
+  mn = s_mn[0];
+  mx = s_mx[0];
+}
+
+template <int K>
+__global__ void __launch_bounds__(kThreads) k_mc_counts(const __grid_constant__ McParams p) {
+  __shared__ unsigned long long s_cnt[kMaxGpus];
+  __shared__ int s_hist[kMaxLenBins + 1];
+  __shared__ int64_t s_mn[kThreads / 32], s_mx[kThreads / 32];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int b = p.b, G = p.G, P = b * G;
+  for (int64_t tr = blockIdx.x; tr < p.ntrials; tr += gridDim.x) {
+    const int32_t* m = p.mat + tr * (int64_t)P;
+    for (int g = t; g < G; g += kThreads) s_cnt[g] = 0ull;
+    __syncthreads();
+    if (p.strategy <= 1) {  // NONE / STRATIFIED: column sums of the (b, G) matrix
+      for (int g = t; g < G; g += kThreads) {
+        long long s = 0;
+        for (int r = 0; r < b; ++r) {
+          const int v = m[(int64_t)r * G + g];
+          if (v < 1 || v > p.max_len) *p.bad = 1;
+          s += v;
+        }
+        s_cnt[g] = (unsigned long long)s;
+      }
+    } else if (p.strategy == 2) {  // LOCAL_PRESORT: one warp per node pool
+      const int gpn = p.gpn, nodes = G / gpn, PP = b * gpn;
+      for (int nd = w; nd < nodes; nd += kThreads / 32) {
+        uint32_t key[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          const int i = lane * K + j;  // pool order: row r, then the node's columns
+          if (i < PP) {
+            const int r = i / gpn, c = i - r * gpn;
+            const int v = m[(int64_t)r * G + nd * gpn + c];
+            if (v < 1 || v > p.max_len) *p.bad = 1;
+            key[j] = (uint32_t)(p.max_len - v);  // ascending key = descending length
+          } else {
+            key[j] = 0xffffffffu;
+          }
+        }
+        warp_bitonic_sort<K>(key, lane);
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          const int pos = lane * K + j;
+          if (pos < PP) {
+            const int r = pos / gpn, c = pos - r * gpn;
+            const int ln = (p.snake && (r & 1)) ? gpn - 1 - c : c;
+            atomicAdd(&s_cnt[nd * gpn + ln], (unsigned long long)(p.max_len - (int)key[j]));
+          }
+        }
+      }
+    } else {  // GLOBAL_PRESORT: counting sort of all b*G values
+      for (int v = t; v <= p.max_len; v += kThreads) s_hist[v] = 0;
+      __syncthreads();
+      for (int i = t; i < P; i += kThreads) {
+        const int v = m[i];
+        if (v < 1 || v > p.max_len) {
+          *p.bad = 1;
+          continue;
+        }
+        atomicAdd(&s_hist[p.max_len - v], 1);  // bin 0 = longest
+      }
+      __syncthreads();
+      if (t == 0) {  // exclusive prefix over <= 4097 bins (one pass, tiny next to the sums)
+        int acc = 0;
+        for (int v = 0; v <= p.max_len; ++v) {
+          const int c = s_hist[v];
+          s_hist[v] = acc;
+          acc += c;
+        }
+      }
+      __syncthreads();
+      for (int pos = t; pos < P; pos += kThreads) {
+        int lo = 0, hi = p.max_len;  // last bin whose start <= pos
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (s_hist[mid] <= pos) lo = mid;
+          else hi = mid - 1;
+        }
+        const int v = p.max_len - lo;
+        const int r = pos / G, c = pos - r * G;
+        const int ln = (p.snake && (r & 1)) ? G - 1 - c : c;
+        atomicAdd(&s_cnt[ln], (unsigned long long)v);
+      }
+    }
+    __syncthreads();
+    int64_t mn = LLONG_MAX, mx = LLONG_MIN;
+    for (int g = t; g < G; g += kThreads) {
+      const int64_t c = (int64_t)s_cnt[g];
+      mn = min(mn, c);
+      mx = max(mx, c);
+      if (p.counts) p.counts[tr * G + g] = c;
+    }
+    block_minmax(mn, mx, s_mn, s_mx);
+    if (t == 0) {
+      p.mins[tr] = mn;
+      p.maxs[tr] = mx;
+    }
+    __syncthreads();
+  }
+}
+
+template <int K>
+int launch(const McParams& p, cudaStream_t st) {
+  const DeviceInfo& di = device_info();
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(p.ntrials, (int64_t)di.sm_count * 8));
+  k_mc_counts<K><<<grid, kThreads, 0, st>>>(p);
+  B2_CHECK(cudaGetLastError());
+  return B2_OK;
+}
+
+}  // namespace
+}  // namespace b2
+
+using namespace b2;
+
+extern "C" int b2_mc_token_counts(const int32_t* mat, int64_t ntrials, int b, int num_gpus, int gpus_per_node,
+                                  int strategy, int scan, int32_t max_len, int64_t* counts, int64_t* mins,
+                                  int64_t* maxs, int32_t* bad, void* stream) {
+  B2_REQUIRE(b >= 1 && num_gpus >= 1 && gpus_per_node >= 1 && num_gpus % gpus_per_node == 0, B2_ERR_INVALID,
+             "bad shape: b=%d G=%d gpn=%d", b, num_gpus, gpus_per_node);
+  B2_REQUIRE(strategy >= 0 && strategy <= 3, B2_ERR_INVALID, "bad strategy %d", strategy);
+  B2_REQUIRE(scan == B2_SCAN_RASTER || scan == B2_SCAN_SNAKE, B2_ERR_INVALID, "bad scan %d", scan);
+  B2_REQUIRE(num_gpus <= kMaxGpus, B2_ERR_UNSUPPORTED, "at most %d GPUs per trial", kMaxGpus);
+  B2_REQUIRE(max_len >= 1 && max_len <= kMaxLenBins, B2_ERR_UNSUPPORTED, "max_len must be in [1, %d]", kMaxLenBins);
+  B2_REQUIRE(strategy != 2 || b * gpus_per_node <= 512, B2_ERR_UNSUPPORTED,
+             "local presort pools of %d samples exceed 512", b * gpus_per_node);
+  B2_REQUIRE(ntrials >= 0, B2_ERR_INVALID, "ntrials must be >= 0");
+  B2_REQUIRE(mins && maxs && bad, B2_ERR_INVALID, "NULL output");
+  cudaStream_t st = (cudaStream_t)stream;
+  B2_CHECK(cudaMemsetAsync(bad, 0, sizeof(int32_t), st));
+  if (ntrials == 0) return B2_OK;
+  B2_REQUIRE(mat, B2_ERR_INVALID, "NULL matrix");
+  McParams p{};
+  p.mat = mat;
+  p.ntrials = ntrials;
+  p.b = b;
+  p.G = num_gpus;
+  p.gpn = gpus_per_node;
+  p.strategy = strategy;
+  p.snake = scan == B2_SCAN_SNAKE;
+  p.max_len = max_len;
+  p.counts = counts;
+  p.mins = mins;
+  p.maxs = maxs;
+  p.bad = bad;
+  const int pp = strategy == 2 ? b * gpus_per_node : 32;
+  if (pp <= 32) return launch<1>(p, st);
+  if (pp <= 64) return launch<2>(p, st);
+  if (pp <= 128) return launch<4>(p, st);
+  if (pp <= 256) return launch<8>(p, st);
+  return launch<16>(p, st);
+}

@@ -15,6 +15,7 @@
 // actually spans (cub::BlockRadixSort), then each sorted slot is dealt to
 // (lane, row) and staged in shared memory so the [lanes][rows] output tile is
 // written with consecutive addresses; token sums read the staged lengths.
+#include "bitonic.cuh"
 #include "common.cuh"
 
 #include <cub/block/block_radix_sort.cuh>
@@ -109,44 +110,6 @@ __global__ void __launch_bounds__(T) k_presort_deal(const __grid_constant__ Pres
 // unstable network yields exactly the reference's stable order whenever the
 // caller does not need input slots (out_pos); ties of identical samples are
 // indistinguishable.  Padding keys (all ones) sort last.
-template <int K>
-__device__ __forceinline__ void warp_bitonic_sort(unsigned long long (&key)[K], int lane) {
-  constexpr int n = 32 * K;
-#pragma unroll
-  for (int size = 2; size <= n; size <<= 1) {
-#pragma unroll
-    for (int d = size >> 1; d > 0; d >>= 1) {
-      if (d >= K) {  // partner in another lane, same slot
-        const int lm = d / K;
-        const bool lower = (lane & lm) == 0;
-#pragma unroll
-        for (int j = 0; j < K; ++j) {
-          const unsigned long long other = __shfl_xor_sync(0xffffffffu, key[j], lm);
-          const int i = lane * K + j;
-          const bool up = (i & size) == 0;
-          const bool take_min = (lower == up);
-          const unsigned long long mn = key[j] < other ? key[j] : other;
-          const unsigned long long mx = key[j] < other ? other : key[j];
-          key[j] = take_min ? mn : mx;
-        }
-      } else {  // both elements in this lane
-#pragma unroll
-        for (int j = 0; j < K; ++j) {
-          if ((j & d) == 0) {
-            const int i = lane * K + j;
-            const bool up = (i & size) == 0;
-            const unsigned long long a = key[j], b = key[j | d];
-            if ((a > b) == up) {
-              key[j] = b;
-              key[j | d] = a;
-            }
-          }
-        }
-      }
-    }
-  }
-}
-
 template <int K, int WARPS>
 __global__ void __launch_bounds__(32 * WARPS) k_presort_deal_warp(const __grid_constant__ PresortParams p) {
   constexpr int n = 32 * K;

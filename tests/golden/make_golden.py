@@ -4,7 +4,7 @@ Run in the build container only (needs /root/reference, read-only):
 
     python tests/golden/make_golden.py
 
-Writes ``tests/golden/h1_golden.npz`` and ``tests/golden/h2_golden.json``.
+Writes ``tests/golden/h1_golden.npz``, ``h2_golden.json`` and ``h2_mc_golden.json``.
 These pin the oracle (``oracle/ddp_oracle.py``) and, through it, the CUDA
 path.  Nothing on the GPU box reads /root/reference; the fixtures travel with
 the repo.
@@ -181,8 +181,38 @@ def h2_cases():
     (OUT / "h2_golden.json").write_text(json.dumps(doc, separators=(",", ":")))
 
 
+def mc_cases():
+    """mcsim: per-trial token counts of every strategy the
+    GPU engine covers, plus the aggregated BalanceStats and one ablation table,
+    all computed by the reference itself."""
+    from ddpsim import mcsim, seqdata
+    from ddpsim.seeding import derive_rng
+
+    n, cseed = 20_000, 606
+    corpus = tuple(seqdata.generate_corpus(seqdata.LengthDistribution(), n, cseed))
+    cases = []
+    for strat, scan, nodes, gpn, lb in (("none", "raster", 2, 4, 16), ("stratified", "raster", 1, 8, 16),
+                                        ("local_presort", "raster", 2, 4, 16), ("local_presort", "snake", 4, 8, 16),
+                                        ("local_presort", "snake", 1, 8, 48), ("global_presort", "raster", 2, 4, 16),
+                                        ("global_presort", "snake", 4, 8, 8)):
+        exp = mcsim.BalanceExperiment(strat, seqdata.Topology(nodes, gpn), corpus, seed=77, local_batch=lb,
+                                      trials=40, scan=scan)
+        prep = mcsim._prepare(exp)
+        tokens = [mcsim._trial_token_counts(derive_rng(77, t), exp, prep).tolist() for t in range(exp.trials)]
+        st = mcsim.run_balance_experiment(exp)
+        cases.append({"strategy": strat, "scan": scan, "nodes": nodes, "gpn": gpn, "lb": lb, "seed": 77,
+                      "trials": exp.trials, "tokens": tokens, "stats": st.__dict__})
+    base = mcsim.BalanceExperiment("local_presort", seqdata.Topology(2, 4), corpus, seed=2402, local_batch=16,
+                                   trials=25)
+    ablation = [[label, st.__dict__] for label, st in mcsim.run_ablation(base)]
+    doc = {"corpus_n": n, "corpus_seed": cseed, "cases": cases,
+           "ablation": {"nodes": 2, "gpn": 4, "lb": 16, "seed": 2402, "trials": 25, "rows": ablation}}
+    (OUT / "h2_mc_golden.json").write_text(json.dumps(doc, separators=(",", ":")))
+
+
 if __name__ == "__main__":
     h1_cases()
     h2_cases()
+    mc_cases()
     for f in sorted(OUT.glob("h*_golden.*")):
         print(f.name, f.stat().st_size)

@@ -1,0 +1,72 @@
+"""Monte-Carlo balance engine on the GPU vs the reference.
+
+Golden per-trial token counts, BalanceStats and an ablation table come from
+running ddpsim.mcsim itself (tests/golden/h2_mc_golden.json); the paper-scale
+case (1,024 GPUs, 10 M corpus) is checked trial by trial against the oracle.
+Integer work: everything is ``==``, including the float statistics (the
+aggregation is the reference's own numpy expression on exact int64 arrays).
+"""
+
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import ddp_oracle as O
+from paper_2402_02447_b200 import Topology
+from paper_2402_02447_b200.mcsim import (BalanceExperiment, _prepare, draw_trials, run_ablation,
+                                         run_balance_experiment, trial_token_counts)
+
+pytestmark = pytest.mark.gpu
+GOLDEN = json.loads((Path(__file__).parent / "golden" / "h2_mc_golden.json").read_text())
+
+
+def _exp(c, lengths, **kw):
+    return BalanceExperiment(c["strategy"], Topology(c["nodes"], c["gpn"]), lengths, seed=c["seed"],
+                             local_batch=c["lb"], trials=c["trials"], scan=c["scan"], **kw)
+
+
+@pytest.mark.parametrize("case", range(len(GOLDEN["cases"])))
+def test_mc_engine_matches_reference_trials_and_stats(case):
+    c = GOLDEN["cases"][case]
+    lengths = O.generate_lengths(GOLDEN["corpus_n"], GOLDEN["corpus_seed"])
+    exp = _exp(c, lengths)
+    prep = _prepare(exp)
+    mat = torch.from_numpy(draw_trials(exp, 0, c["trials"], prep=prep)).cuda()
+    mins, maxs, cnt, bad = trial_token_counts(exp, mat, prep.max_len, counts=True)
+    assert int(bad) == 0
+    assert cnt.cpu().tolist() == c["tokens"]
+    assert mins.cpu().tolist() == [min(t) for t in c["tokens"]]
+    assert maxs.cpu().tolist() == [max(t) for t in c["tokens"]]
+    st = run_balance_experiment(exp, chunk=7)  # several chunks: the double-buffered pipeline
+    assert st.__dict__ == c["stats"]
+
+
+def test_mc_ablation_matches_reference():
+    a = GOLDEN["ablation"]
+    lengths = O.generate_lengths(GOLDEN["corpus_n"], GOLDEN["corpus_seed"])
+    base = BalanceExperiment("local_presort", Topology(a["nodes"], a["gpn"]), lengths, seed=a["seed"],
+                             local_batch=a["lb"], trials=a["trials"])
+    rows = run_ablation(base)
+    assert [[label, st.__dict__] for label, st in rows] == a["rows"]
+
+
+@pytest.mark.parametrize("strategy,scan", [("local_presort", "snake"), ("global_presort", "raster"),
+                                           ("stratified", "raster")])
+def test_mc_engine_paper_scale_vs_oracle(strategy, scan):
+    """1,024 GPUs (128 nodes x 8), lb 16, the 10 M corpus: 64 trials on the GPU,
+    trials 0, 31 and 63 recomputed by the oracle."""
+    lengths = O.generate_lengths(10_000_000, 2402)
+    exp = BalanceExperiment(strategy, Topology(128, 8), lengths, seed=99, local_batch=16, trials=64, scan=scan)
+    prep = _prepare(exp)
+    mat = torch.from_numpy(draw_trials(exp, 0, 64, prep=prep)).cuda()
+    mins, maxs, cnt, bad = trial_token_counts(exp, mat, prep.max_len, counts=True)
+    assert int(bad) == 0
+    cnt = cnt.cpu().numpy()
+    for t in (0, 31, 63):
+        ref = O.mcsim_trial_counts(strategy, lengths, O.DEFAULT_BOUNDS, 16, 128, 8, scan == "snake", 99, t)
+        assert cnt[t].tolist() == ref.tolist(), t
+    assert np.array_equal(mins.cpu().numpy(), cnt.min(axis=1))
+    assert np.array_equal(maxs.cpu().numpy(), cnt.max(axis=1))

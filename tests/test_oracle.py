@@ -148,3 +148,27 @@ def test_h2_mcsim_second_oracle(h2_golden):
     for c in h2_golden["mcsim"]:
         tok = O.mcsim_local_presort_tokens(c["mat"], c["nodes"], c["gpn"], c["scan"] == "snake")
         assert tok.tolist() == c["tokens"]
+
+
+# ---------------------------------------------------------------------------
+# mcsim: the oracle vs the reference's own trials
+
+def _mc_golden():
+    import json
+    from pathlib import Path
+
+    return json.loads((Path(__file__).parent / "golden" / "h2_mc_golden.json").read_text())
+
+
+def test_oracle_mcsim_trials_and_stats_match_reference():
+    g = _mc_golden()
+    lengths = O.generate_lengths(g["corpus_n"], g["corpus_seed"])
+    for c in g["cases"]:
+        mins, maxs = [], []
+        for t in range(c["trials"]):
+            tok = O.mcsim_trial_counts(c["strategy"], lengths, O.DEFAULT_BOUNDS, c["lb"], c["nodes"], c["gpn"],
+                                       c["scan"] == "snake", c["seed"], t)
+            assert tok.tolist() == c["tokens"][t], (c["strategy"], c["scan"], t)
+            mins.append(tok.min())
+            maxs.append(tok.max())
+        assert O.mcsim_stats(mins, maxs) == c["stats"], c["strategy"]
