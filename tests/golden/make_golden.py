@@ -210,9 +210,29 @@ def mc_cases():
     (OUT / "h2_mc_golden.json").write_text(json.dumps(doc, separators=(",", ":")))
 
 
+def timeline_cases():
+    """timeline.schedule totals (timeline.py:97-152) for seeded random plans:
+    pins the restated model in tools/timeline_calibrate.py."""
+    from ddpsim import timeline
+
+    rng = np.random.default_rng(8)
+    cases = []
+    for B in (1, 2, 5, 37, 52):
+        for scale in (0.1, 1.0, 10.0):
+            plan = timeline.TimelinePlan(t_comp=tuple(rng.uniform(0.5, 3, B)), t_comm=tuple(rng.uniform(0, 1, B) * scale),
+                                         t_clip=tuple(rng.uniform(0, 0.1, B)), t_gclip=float(rng.uniform(0, 2)),
+                                         t_nred=float(rng.uniform(0, 0.5)))
+            cases.append({"t_comp": list(plan.t_comp), "t_comm": list(plan.t_comm), "t_clip": list(plan.t_clip),
+                          "t_gclip": plan.t_gclip, "t_nred": plan.t_nred,
+                          "total": {m: timeline.schedule(plan, m).total
+                                    for m in ("bucket_wise", "after_allreduce", "before_allreduce")}})
+    (OUT / "timeline_golden.json").write_text(json.dumps(cases))
+
+
 if __name__ == "__main__":
     h1_cases()
     h2_cases()
     mc_cases()
+    timeline_cases()
     for f in sorted(OUT.glob("h*_golden.*")):
         print(f.name, f.stat().st_size)

@@ -140,3 +140,19 @@ def test_draw_batch_golden(h2_golden):
                 assert str(ei.value) == expect["error"]
                 break
             assert [s.id for s in B.draw_batch(st, al, seed=1000 + step)] == expect
+
+
+def test_timeline_model_restatement_matches_reference_golden():
+    """tools/timeline_calibrate.schedule_total == ddpsim timeline.schedule (golden, timeline.py:97-152)."""
+    import importlib.util
+    import json
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    spec = importlib.util.spec_from_file_location("tc", root / "tools" / "timeline_calibrate.py")
+    tc = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(tc)
+    for c in json.loads((root / "tests" / "golden" / "timeline_golden.json").read_text()):
+        for mode, total in c["total"].items():
+            got = tc.schedule_total(c["t_comp"], c["t_comm"], c["t_clip"], c["t_gclip"], c["t_nred"], mode)
+            assert got == total, (mode, got, total)
