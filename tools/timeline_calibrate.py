@@ -42,16 +42,21 @@ def schedule_total(t_comp, t_comm, t_clip, t_gclip, t_nred, mode: str) -> float:
     order = range(B - 1, -1, -1)  # bucket B first
     ready = [0.0] * B
     t = 0.0
+    # same float operation order as the reference (bits match its totals)
     if mode == "bucket_wise":
         for b in order:
-            t += t_comp[b] + t_clip[b]
+            t = t + t_comp[b]
+            t = t + t_clip[b]
             ready[b] = t
     elif mode == "after_allreduce":
         for b in order:
-            t += t_comp[b]
+            t = t + t_comp[b]
             ready[b] = t
     else:  # before_allreduce
-        t = sum(t_comp) + t_nred + t_gclip
+        for b in order:
+            t = t + t_comp[b]
+        t = t + t_nred
+        t = t + t_gclip
         ready = [t] * B
     end = 0.0
     first_end = None
