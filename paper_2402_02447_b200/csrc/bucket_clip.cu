@@ -917,6 +917,10 @@ int launch_clip_k1(ClipParams& p, cudaStream_t stream) {
       case 29: return launch_ws<Tin, Tout, 224, 288, 2, 1, 8, 4>(p, stream);
       case 30: return launch_ws<Tin, Tout, 192, 320, 2, 1, 8, 2>(p, stream);
       case 31: return launch_ws<Tin, Tout, 192, 320, 2, 1, 12, 4>(p, stream);
+      case 32: return launch_ws<Tin, Tout, 192, 320, 2, 0, 8, 4>(p, stream);
+      case 33: return launch_ws<Tin, Tout, 192, 320, 2, 2, 8, 4>(p, stream);
+      case 34: return launch_ws<Tin, Tout, 384, 640, 1, 1, 8, 4>(p, stream);
+      case 35: return launch_ws<Tin, Tout, 192, 320, 2, 1, 8, 8>(p, stream);
       default: break;
     }
   }

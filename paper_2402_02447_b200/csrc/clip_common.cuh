@@ -215,6 +215,12 @@ inline int choose_groups(const ClipParams& p, int grid, size_t in_elem_bytes) {
   const size_t budget = 24u << 20;  // bytes of buckets in flight across groups (x2 for the lag)
   int r = (int)std::max<size_t>(1, budget / std::max<size_t>(avg, 1));
   r = std::min(r, std::max(1, grid / 4));  // >= 4 CTAs per group
+  static int forced = -1;  // B2_CLIP_GROUPS: override for A/B runs
+  if (forced < 0) {
+    const char* e = getenv("B2_CLIP_GROUPS");
+    forced = e ? atoi(e) : 0;
+  }
+  if (forced > 0) r = forced;
   r = std::min(r, p.nseg);
   return r;
 }
