@@ -338,20 +338,20 @@ def bench_clip(args, rank, world, local):
     host.copy_(g.view(1, -1).cpu())
     e2e_steps = max(2, min(args.steps, 5))
     if world == 1:
-        def e2e_step():
-            st = B.GradientState(host, layout)
-            return B.sync_bucketwise(st, cfg)
+        out_f32 = torch.empty(dim, dtype=torch.float32, pin_memory=True)
+
+        def e2e_step():  # the host-resident form of GradientState + sync_bucketwise, streamed per bucket
+            return B.sync_bucketwise_host(host, layout, cfg, out=out_f32)
         d2h = dim * 4
-        api = "GradientState + sync_bucketwise (pinned host fp32 in, host fp32 out)"
+        api = ("sync_bucketwise_host (= GradientState + sync_bucketwise; pinned host fp32 in, host fp32 out; "
+               "H2D / K1 / D2H streamed per bucket)")
     else:
         out_host = torch.empty(dim, dtype=torch.bfloat16, pin_memory=True)
         if launches_per_step == 1:
             def e2e_step():
-                dg = host.view(-1).to("cuda", non_blocking=True)
-                out_host.copy_(fsync.sync(dg), non_blocking=True)
-                torch.cuda.current_stream().synchronize()
-                return out_host
-            api = "FusedBucketSync.sync (pinned host fp32 in, host bf16 out)"
+                return fsync.sync_host(host.view(-1), out=out_host)
+            api = ("FusedBucketSync.sync_host (pinned host fp32 in, host bf16 out; H2D / K4 / D2H "
+                   "streamed per 4-bucket chunk)")
         else:
             def e2e_step():
                 dg = host.view(-1).to("cuda", non_blocking=True)

@@ -20,6 +20,7 @@ from .gradsync import (
     sync_after,
     sync_before,
     sync_bucketwise,
+    sync_bucketwise_host,
     synchronize,
 )
 from .seqdata import (
@@ -53,7 +54,7 @@ __all__ = [
     "Assignment", "ScanPattern", "assign_global_presort", "assign_local_presort", "presort_deal",
     "BucketClipper", "ClipConfig", "ClipMode", "GradientState", "allreduce_mean",
     "capped_bucket_layout", "clip_by_norm", "equal_bucket_layout", "gradient_state_from_dict",
-    "sync_after", "sync_before", "sync_bucketwise", "synchronize",
+    "sync_after", "sync_before", "sync_bucketwise", "sync_bucketwise_host", "synchronize",
     "DEFAULT_BIN_BOUNDARIES", "DEFAULT_BIN_PROBS", "MAX_SEQ_LEN", "LengthDistribution",
     "Sample", "Topology", "generate_corpus", "generate_lengths",
     "DeviceStrata", "Strata", "StratumAllocation", "allocate_counts", "draw_batch",

@@ -335,6 +335,68 @@ class FusedBucketSync:
             _lib.check(rc)
         return self.stage
 
+    def sync_host(self, grad_host: torch.Tensor, out: torch.Tensor | None = None, chunk_buckets: int = 4):
+        """Host-resident step: pinned fp32 gradient in, averaged clipped bf16 gradient out (host).
+
+        Streams chunks of ``chunk_buckets`` consecutive buckets in backward
+        order (gradsync.py:157): host->device copy of chunk k+1, one fused K4
+        launch on chunk k and device->host copy of chunk k-1 run at once on
+        three streams (both PCIe directions and NVLink busy together).  Every
+        rank issues the same launch sequence, so the chunks pair up across
+        ranks.  Returns the host tensor (``out`` or a new pinned one).
+        """
+        if grad_host.numel() != self.dim or grad_host.dtype != torch.float32 or grad_host.is_cuda:
+            raise ValueError(f"expected a host float32 gradient of {self.dim} elements")
+        g = grad_host.reshape(-1)
+        if out is None:
+            out = torch.empty(self.dim, dtype=torch.bfloat16, pin_memory=True)
+        if getattr(self, "_dev_in", None) is None:
+            self._dev_in = torch.empty(self.dim, dtype=torch.float32, device=self.device)
+            self._h2d, self._d2h = torch.cuda.Stream(self.device), torch.cuda.Stream(self.device)
+        chunks = self._host_chunks(chunk_buckets)
+        compute = torch.cuda.current_stream(self.device)
+        ws = self.clipper.workspace
+        sp = _lib.stream_ptr(compute)
+        self._h2d.wait_stream(compute)  # the previous step's reads of _dev_in are done
+        for c0, n, offs, lens, a, b in chunks:
+            with torch.cuda.stream(self._h2d):
+                self._dev_in[a:b].copy_(g[a:b], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self._h2d)
+            compute.wait_event(ev)
+            if self.mc:
+                rc = self.lib.b2_bucket_clip_allreduce_nvls(
+                    self._dev_in.data_ptr(), self._stages, self.mc, self._flags, self.world, self.rank, offs, lens,
+                    n, float(self.limit), self._norms_call[c0:].data_ptr(), None, ws.data_ptr(), ws.numel(), sp)
+            else:
+                rc = self.lib.b2_bucket_clip_allreduce_p2p(
+                    self._dev_in.data_ptr(), self._stages, self._flags, self.world, self.rank, offs, lens, n,
+                    float(self.limit), self._norms_call[c0:].data_ptr(), None, ws.data_ptr(), ws.numel(), sp)
+            _lib.check(rc)
+            ev2 = torch.cuda.Event()
+            ev2.record(compute)
+            self._d2h.wait_event(ev2)
+            with torch.cuda.stream(self._d2h):
+                out[a:b].copy_(self.stage[a:b], non_blocking=True)
+        compute.wait_stream(self._d2h)
+        compute.synchronize()
+        return out
+
+    def _host_chunks(self, chunk_buckets: int):
+        cache = getattr(self, "_hchunks", {})
+        if chunk_buckets not in cache:
+            order = list(reversed(range(len(self.layout))))
+            step = max(1, min(int(chunk_buckets), 128))
+            res = []
+            for c0 in range(0, len(order), step):
+                part = order[c0:c0 + step]  # descending bucket indices: one contiguous range
+                a, b = self.layout[part[-1]][0], self.layout[part[0]][1]
+                res.append((c0, len(part), _lib.i64_array(self.layout[q][0] for q in part),
+                            _lib.i64_array(self.layout[q][1] - self.layout[q][0] for q in part), a, b))
+            cache[chunk_buckets] = res
+            self._hchunks = cache
+        return cache[chunk_buckets]
+
     @property
     def norms(self) -> torch.Tensor:
         """This rank's per-bucket norms, in layout order."""

@@ -350,6 +350,92 @@ def _clip_then_mean(state: GradientState, layout, limit: float):
     return _result(out, state._host)
 
 
+def _check_layout(layout, dim: int) -> tuple:
+    layout = tuple((int(a), int(b)) for a, b in layout)
+    if not layout:
+        raise ValueError("bucket_layout must have at least one bucket")
+    edge = 0
+    for a, b in layout:
+        if a != edge or b <= a:
+            raise ValueError(f"bucket_layout must be disjoint contiguous ranges covering [0, {dim}), got {layout}")
+        edge = b
+    if edge != dim:
+        raise ValueError(f"bucket_layout covers [0, {edge}), expected [0, {dim})")
+    return layout
+
+
+def sync_bucketwise_host(workers, bucket_layout, cfg: ClipConfig, out: torch.Tensor | None = None):
+    """Host-resident fast path of ``sync_bucketwise(GradientState(workers, layout), cfg)``.
+
+    Same validation, errors and result as the two reference calls
+    (gradsync.py:43-78, 148-162), but streamed bucket by bucket in the
+    reference's reverse order over three CUDA streams — host->device copy of
+    bucket b, K1 clip of b (with its non-finite flag), device->host copy of
+    b — so both PCIe directions run at once instead of one after the other.
+    A non-finite input raises ``ValueError`` ("gradient state has non-finite
+    components") before any result is returned.  ``out`` may be a pinned
+    host tensor to receive the result (else a pinned one is allocated); the
+    host input should be pinned for full PCIe rate.  Single worker (K = 1);
+    K > 1 goes through GradientState + sync_bucketwise.
+    """
+    _require_mode(cfg, ClipMode.BUCKET_WISE)
+    src = workers if isinstance(workers, torch.Tensor) else torch.from_numpy(
+        np.ascontiguousarray(np.asarray(workers, dtype=float)))
+    if src.ndim != 2 or src.shape[0] < 1 or src.shape[1] < 1:
+        raise ValueError(f"expected a (workers, dim) matrix, got shape {tuple(src.shape)}")
+    if src.is_cuda or src.shape[0] != 1:
+        return sync_bucketwise(GradientState(workers, bucket_layout), cfg)
+    if src.dtype not in (torch.float32, torch.float64):
+        src = src.to(torch.float64)
+    _lib.load()
+    D = src.shape[1]
+    layout = _check_layout(bucket_layout, D)
+    limit = cfg.threshold / math.sqrt(len(layout))
+    g = src.reshape(-1)
+    if not g.is_contiguous():
+        g = g.contiguous()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    compute = torch.cuda.current_stream(dev)
+    h2d, d2h = _host_streams(dev)
+    d_in = torch.empty(D, dtype=g.dtype, device=dev)
+    d_out = torch.empty(D, dtype=g.dtype, device=dev)
+    if out is None:
+        out = torch.empty(D, dtype=g.dtype, pin_memory=True)
+    elif out.numel() != D or out.dtype != g.dtype:
+        raise ValueError(f"out must be a host {g.dtype} tensor of {D} elements")
+    flags = torch.empty(len(layout), dtype=torch.int32, device=dev)
+    c = _clipper()
+    h2d.wait_stream(compute)  # d_in / d_out are fresh allocations of the compute stream
+    for j, (a, b) in enumerate(reversed(layout)):  # bucket B first (:157)
+        with torch.cuda.stream(h2d):
+            d_in[a:b].copy_(g[a:b], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(h2d)
+        compute.wait_event(ev)
+        c.clip_cast(d_in, d_out, [(a, a, b - a)], limit, nonfinite=flags[j:j + 1])
+        ev2 = torch.cuda.Event()
+        ev2.record(compute)
+        d2h.wait_event(ev2)
+        with torch.cuda.stream(d2h):
+            out[a:b].copy_(d_out[a:b], non_blocking=True)
+    compute.wait_stream(d2h)
+    d_in.record_stream(h2d)
+    d_out.record_stream(d2h)
+    if bool(flags.any()):  # synchronises: every copy has landed
+        raise ValueError("gradient state has non-finite components")
+    return out.numpy()
+
+
+_host_stream_cache: dict = {}
+
+
+def _host_streams(dev):
+    s = _host_stream_cache.get(dev.index)
+    if s is None:
+        s = _host_stream_cache[dev.index] = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+    return s
+
+
 _SYNC_FNS = {
     ClipMode.AFTER_ALLREDUCE: sync_after,
     ClipMode.BEFORE_ALLREDUCE: sync_before,

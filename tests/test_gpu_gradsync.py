@@ -270,3 +270,39 @@ def test_bert_sized_parity(dim):
         if cf < 1.0:
             assert abs(np.linalg.norm(o32[a:b].astype(np.float64)) - limit) <= 1e-5 * limit
     assert np.linalg.norm(o32.astype(np.float64)) <= 1.0 * (1 + 1e-5)
+
+
+def test_sync_bucketwise_host_streamed_matches_reference():
+    """sync_bucketwise_host == sync_bucketwise(GradientState(...)) for host input:
+    same result (within fp32 tolerance of the fp64 oracle), same errors."""
+    from paper_2402_02447_b200 import sync_bucketwise_host
+
+    rng = np.random.default_rng(31)
+    for D, B in ((1000, 3), (4099, 7), (262144, 16)):
+        w = rng.standard_normal((1, D)) * rng.choice([1e-3, 1.0, 1e3], size=(1, D))
+        layout = equal_bucket_layout(D, B)
+        ref = O.sync_bucketwise(w, layout, 1.0)
+        cfg = ClipConfig(1.0, "bucket_wise")
+        # fp64 numpy input (the reference's own call shape)
+        got = sync_bucketwise_host(w, layout, cfg)
+        assert got.dtype == np.float64
+        assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+        # pinned fp32 tensor input
+        w32 = torch.from_numpy(w.astype(np.float32)).pin_memory()
+        got32 = sync_bucketwise_host(w32, layout, cfg)
+        assert np.abs(got32 - ref).max() <= 1e-5 * np.abs(ref).max()
+        same = sync_bucketwise(GradientState(w32, layout), cfg)
+        assert np.abs(got32 - same).max() <= 1e-6 * np.abs(ref).max()
+    bad = np.ones((1, 100))
+    bad[0, 57] = np.nan
+    with pytest.raises(ValueError, match="non-finite"):
+        sync_bucketwise_host(bad, equal_bucket_layout(100, 4), ClipConfig(1.0, "bucket_wise"))
+    with pytest.raises(ValueError, match="mode"):
+        sync_bucketwise_host(np.ones((1, 8)), equal_bucket_layout(8, 2), ClipConfig(1.0, "after_allreduce"))
+    with pytest.raises(ValueError, match="bucket_layout"):
+        sync_bucketwise_host(np.ones((1, 8)), ((0, 3), (4, 8)), ClipConfig(1.0, "bucket_wise"))
+    # K > 1 takes the GradientState path, same answer as the reference
+    w2 = rng.standard_normal((3, 500))
+    got2 = sync_bucketwise_host(w2, equal_bucket_layout(500, 5), ClipConfig(1.0, "bucket_wise"))
+    ref2 = O.sync_bucketwise(w2, equal_bucket_layout(500, 5), 1.0)
+    assert np.abs(got2 - ref2).max() <= 1e-12 * np.abs(ref2).max()

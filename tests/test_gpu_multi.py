@@ -66,6 +66,10 @@ def _fused_worker(rank, world, port, q, transport="p2p"):
             graph.replay()
         torch.cuda.synchronize()
         outs.append(sync.stage.float().cpu().numpy())
+        # host-resident streamed step (H2D / K4 per chunk / D2H), several chunk sizes
+        gh = g.cpu().pin_memory()
+        for cb in (1, 3, 128):
+            outs.append(sync.sync_host(gh, chunk_buckets=cb).float().numpy())
         res = {"outs": outs, "norms": sync.norms.cpu().numpy()}
         sync.close()
         q.put((rank, res))
