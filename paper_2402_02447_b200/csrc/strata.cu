@@ -8,8 +8,11 @@
 // algorithmic: 4 B length read, 4 B id written; +4 B if explicit ids are read):
 //   k_strata_count  : one CTA per 4096-key tile -> per-tile per-stratum counts
 //                     (+ the shard's first bad index via atomicMin)
-//   k_strata_scatter: one CTA per tile sums the counts of the earlier tiles of
-//                     its shard (one L2 round trip instead of a scan launch),
+//                     and, in the LAST tile of each shard to finish (atomic
+//                     ticket), the shard's exclusive per-tile prefixes (in
+//                     place over the tile counts) and per-stratum totals —
+//                     no scan launch, no O(tiles^2) re-summing
+//   k_strata_scatter: one CTA per tile reads its prefix row + the shard totals,
 //                     then places its keys with stable in-tile ranks from a
 //                     single packed block scan (4 strata x 16-bit fields per
 //                     u64), staged through shared memory so each stratum's run
@@ -38,7 +41,8 @@ struct StrataParams {
   int32_t bounds[kMaxStrata];
   int64_t shard_off[kMaxShards + 1];  // element offset of each shard
   int32_t tile_off[kMaxShards + 1];   // first tile of each shard
-  int32_t* tile_counts;               // [T][kMaxStrata]
+  int32_t* tile_counts;               // [T][kMaxStrata]: counts, then exclusive in-shard prefixes
+  unsigned* shard_done;               // [kMaxShards] tiles counted per shard (zeroed per launch)
   int64_t* counts;                    // [nshard][nb] totals
   int64_t* bad;                       // [nshard] first bad index within the shard (u64 min), pre-set to -1
   int32_t* ids_out;                   // same offsets as the input
@@ -123,6 +127,40 @@ __global__ void __launch_bounds__(kT) k_strata_count(const __grid_constant__ Str
   }
   __syncthreads();
   if (threadIdx.x < NB) p.tile_counts[(int64_t)tile * kMaxStrata + threadIdx.x] = threadIdx.x < p.nb ? cnt[threadIdx.x] : 0;
+
+  // the shard's last tile to finish turns its tile counts into exclusive
+  // prefixes (in place) and publishes the shard totals
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned nt = (unsigned)(p.tile_off[g + 1] - p.tile_off[g]);
+    s_last = atomicAdd(&p.shard_done[g], 1u) == nt - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int t0 = p.tile_off[g], t1 = p.tile_off[g + 1], nt = t1 - t0;
+  const int per = (nt + kT - 1) / kT;  // contiguous tiles per thread
+  const int a = min(t0 + (int)threadIdx.x * per, t1), b = min(a + per, t1);
+  using Scan = cub::BlockScan<int, kT>;
+  __shared__ typename Scan::TempStorage scan;
+  __shared__ int64_t s_tot[NB];
+  for (int k = 0; k < NB; ++k) {
+    int sum = 0;
+    for (int t = a; t < b; ++t) sum += __ldcg(&p.tile_counts[(int64_t)t * kMaxStrata + k]);
+    int ex, agg;
+    Scan(scan).ExclusiveSum(sum, ex, agg);
+    for (int t = a; t < b; ++t) {
+      int32_t* c = &p.tile_counts[(int64_t)t * kMaxStrata + k];
+      const int v = __ldcg(c);
+      *c = ex;
+      ex += v;
+    }
+    if (threadIdx.x == 0) s_tot[k] = agg;
+    __syncthreads();  // scan storage reuse
+  }
+  if (threadIdx.x < p.nb) p.counts[(int64_t)g * p.nb + threadIdx.x] = s_tot[threadIdx.x];
 }
 
 // pass 2: each tile sums the counts of the earlier tiles of its shard (one L2
@@ -146,40 +184,11 @@ __global__ void __launch_bounds__(kT) k_strata_scatter(const __grid_constant__ S
   const int64_t sbeg = p.shard_off[g], send = p.shard_off[g + 1];
   const int64_t lbase = (int64_t)(tile - p.tile_off[g]) * kTile;
   const int valid = (int)min64(kTile, send - sbeg - lbase);
-  if (threadIdx.x < kMaxStrata) {
-    s_pre[threadIdx.x] = 0ull;
-    s_tot[threadIdx.x] = 0ull;
+  if (threadIdx.x < kMaxStrata) {  // this tile's exclusive prefix + the shard totals (from pass 1)
+    const bool in = threadIdx.x < p.nb;
+    s_pre[threadIdx.x] = in ? (unsigned long long)p.tile_counts[(int64_t)tile * kMaxStrata + threadIdx.x] : 0ull;
+    s_tot[threadIdx.x] = in ? (unsigned long long)p.counts[(int64_t)g * p.nb + threadIdx.x] : 0ull;
   }
-  __syncthreads();
-  {  // prefix over earlier tiles + shard totals, per stratum
-    unsigned long long pre[NB], tot[NB];
-#pragma unroll
-    for (int k = 0; k < NB; ++k) pre[k] = tot[k] = 0ull;
-    for (int t2 = p.tile_off[g] + threadIdx.x; t2 < p.tile_off[g + 1]; t2 += kT) {
-#pragma unroll
-      for (int k = 0; k < NB; ++k) {
-        const unsigned long long cnt = (unsigned long long)p.tile_counts[(int64_t)t2 * kMaxStrata + k];
-        tot[k] += cnt;
-        if (t2 < tile) pre[k] += cnt;
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < NB; ++k) {
-      {
-        unsigned long long a = pre[k], b = tot[k];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          a += __shfl_xor_sync(0xffffffffu, a, o);
-          b += __shfl_xor_sync(0xffffffffu, b, o);
-        }
-        if ((threadIdx.x & 31) == 0) {
-          if (a) atomicAdd(&s_pre[k], a);
-          if (b) atomicAdd(&s_tot[k], b);
-        }
-      }
-    }
-  }
-
   int32_t v[kItems];
   LoadT(sm.ld).Load(p.len + sbeg + lbase, v, valid, 1);
   __syncthreads();
@@ -216,7 +225,6 @@ __global__ void __launch_bounds__(kT) k_strata_scatter(const __grid_constant__ S
       acc += (int)agg.field(k);
       s_dst[k] = gbase + (int64_t)s_pre[k];
       gbase += (int64_t)s_tot[k];
-      if (tile == p.tile_off[g]) p.counts[(int64_t)g * p.nb + k] = (int64_t)s_tot[k];
     }
     s_lstart[p.nb] = acc;
   }
@@ -257,8 +265,8 @@ static inline int64_t strata_tiles(int64_t n) { return (n + kTile - 1) / kTile; 
 
 extern "C" size_t b2_strata_workspace_bytes(int64_t n) {
   if (n < 1) n = 1;
-  // per-tile counts; + one partial tile per shard boundary
-  return (size_t)(strata_tiles(n) + kMaxShards) * kMaxStrata * sizeof(int32_t);
+  // per-shard tile tickets; per-tile counts (+ one partial tile per shard boundary)
+  return kMaxShards * sizeof(unsigned) + (size_t)(strata_tiles(n) + kMaxShards) * kMaxStrata * sizeof(int32_t);
 }
 
 extern "C" int b2_strata_partition_shards(const int32_t* lengths, const int32_t* ids, const int64_t* shard_off,
@@ -287,14 +295,16 @@ extern "C" int b2_strata_partition_shards(const int32_t* lengths, const int32_t*
     T += strata_tiles(n);
   }
   p.tile_off[nshard] = (int32_t)T;
-  B2_REQUIRE(workspace && workspace_bytes >= (size_t)T * kMaxStrata * sizeof(int32_t), B2_ERR_INVALID,
-             "strata workspace needs %zu bytes", (size_t)T * kMaxStrata * sizeof(int32_t));
-  p.tile_counts = static_cast<int32_t*>(workspace);
+  const size_t need = kMaxShards * sizeof(unsigned) + (size_t)T * kMaxStrata * sizeof(int32_t);
+  B2_REQUIRE(workspace && workspace_bytes >= need, B2_ERR_INVALID, "strata workspace needs %zu bytes", need);
+  p.shard_done = static_cast<unsigned*>(workspace);
+  p.tile_counts = reinterpret_cast<int32_t*>(static_cast<char*>(workspace) + kMaxShards * sizeof(unsigned));
   p.counts = counts;
   p.bad = bad;
   p.ids_out = ids_out;
   cudaStream_t st = (cudaStream_t)stream;
   B2_CHECK(cudaMemsetAsync(bad, 0xff, sizeof(int64_t) * nshard, st));
+  B2_CHECK(cudaMemsetAsync(p.shard_done, 0, sizeof(unsigned) * nshard, st));
   if (nb <= 4) {
     k_strata_count<4><<<(unsigned)T, kT, 0, st>>>(p);
     B2_CHECK(cudaGetLastError());
