@@ -566,7 +566,8 @@ def bench_mcsim(args, lens):
     import torch
 
     from paper_2402_02447_b200 import Topology
-    from paper_2402_02447_b200.mcsim import BalanceExperiment, _prepare, draw_trials, run_trials, trial_token_counts
+    from paper_2402_02447_b200.mcsim import (BalanceExperiment, _prepare, draw_trials, draw_trials_device, run_trials,
+                                             trial_token_counts)
 
     T = args.mc_trials
     exp = BalanceExperiment("local_presort", Topology(128, 8), lens, seed=CORPUS_SEED, local_batch=16, trials=T,
@@ -579,8 +580,19 @@ def bench_mcsim(args, lens):
     t0 = time.perf_counter()
     mat = draw_trials(exp, 0, n_d, prep=prep, threads=threads)
     t_draw = time.perf_counter() - t0
+    # device draws alone (one warp per trial, CUDA events)
+    pools = torch.from_numpy(prep.pools).cuda()
+    dmat = torch.empty((n_d, keys_per_trial), dtype=torch.int32, device="cuda")
+    draw_trials_device(exp, 0, n_d, out=dmat, prep=prep, pools=pools)
+    torch.cuda.synchronize()
+    evd = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    evd[0].record()
+    draw_trials_device(exp, 0, n_d, out=dmat, prep=prep, pools=pools)
+    evd[1].record()
+    torch.cuda.synchronize()
+    t_ddraw = evd[0].elapsed_time(evd[1]) * 1e-3
+    same = bool(np.array_equal(dmat.cpu().numpy(), mat))
     # kernel alone (device-resident matrices, CUDA events)
-    dmat = torch.from_numpy(mat).cuda()
     for _ in range(3):
         trial_token_counts(exp, dmat, prep.max_len)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -603,6 +615,10 @@ def bench_mcsim(args, lens):
             "avg_min": float(mins.mean()), "avg_max": float(maxs.mean()),
             "draws": {"keys_per_s": n_d * keys_per_trial / t_draw, "threads": threads,
                       "impl": "b2_mc_draw (bit-exact numpy SeedSequence/PCG64/choice port, host C++)"},
+            "draws_device": {"keys_per_s": n_d * keys_per_trial / t_ddraw, "ms_per_4096_trials": t_ddraw * 1e3,
+                             "bit_identical_to_host": same,
+                             "impl": "b2_mc_draw_device (same port on the GPU, one warp per trial)"},
+            "e2e_draws": "device (every stratum in numpy's Floyd branch)",
             "kernel": {"keys_per_s": n_d * keys_per_trial / t_k, "ms_per_4096_trials": t_k * 1e3,
                        "achieved_gbs": kbytes / t_k / 1e9, "frac": kbytes / t_k / 1e9 / peaks()["hbm_gbs"],
                        "bytes_per_key": 4}}

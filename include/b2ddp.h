@@ -232,6 +232,16 @@ int b2_presort_deal(const int32_t* ids, const int32_t* lens, int64_t nseg, int s
 int b2_mc_draw(const int32_t* lengths, const int64_t* pool_sizes, int nstrata, const int64_t* counts,
                int num_gpus, uint64_t seed, int64_t first_trial, int64_t ntrials, int nthreads, int32_t* out);
 
+/* Monte-Carlo trial draws ON THE DEVICE: the same bit-exact draws as
+ * b2_mc_draw (derive_rng(seed, t), choice(replace=False) Floyd branch +
+ * shuffle), one warp per trial.  pool_lens is device memory (strata
+ * concatenated), out is device [ntrials][b*num_gpus].  A stratum in numpy's
+ * tail-shuffle branch (pop > 10000 and need > pop/50) -> B2_ERR_UNSUPPORTED
+ * (use b2_mc_draw). */
+int b2_mc_draw_device(const int32_t* pool_lens, const int64_t* pool_sizes, int nstrata, const int64_t* counts,
+                      int num_gpus, uint64_t seed, int64_t first_trial, int64_t ntrials, int32_t* out,
+                      void* stream);
+
 /* Monte-Carlo balance engine, device side: per-trial per-GPU token counts
  * and their min/max (mcsim._trial_token_counts :182-213, _run :284-300).
  * strategy: 0 NONE, 1 STRATIFIED (column sums), 2 LOCAL_PRESORT (per-node

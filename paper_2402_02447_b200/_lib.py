@@ -67,6 +67,7 @@ SIGNATURES = {
     ),
     "b2_mc_draw": (_I, [_P, _P, _I, _P, _I, C.c_uint64, _I64, _I64, _I, _P]),
     "b2_mc_token_counts": (_I, [_P, _I64, _I, _I, _I, _I, _I, C.c_int32, _P, _P, _P, _P, _P]),
+    "b2_mc_draw_device": (_I, [_P, _P, _I, _P, _I, C.c_uint64, _I64, _I64, _P, _P]),
 }
 
 _lock = threading.Lock()

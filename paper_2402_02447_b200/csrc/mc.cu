@@ -17,7 +17,9 @@
 // whose descending positions are resolved by binary search.
 #include "bitonic.cuh"
 #include "common.cuh"
+#include "rng.h"
 
+#include <algorithm>
 #include <climits>
 
 namespace b2 {
@@ -167,10 +169,134 @@ int launch(const McParams& p, cudaStream_t st) {
   return B2_OK;
 }
 
+// ---------------------------------------------------------------- device draws
+// Trial t's draws (derive_rng(seed, t); per stratum choice(pool, need,
+// replace=False) in the Floyd branch + numpy's final shuffle) for many trials
+// at once: one warp per trial.  Floyd's algorithm is a sequential chain of
+// bounded draws, so lane 0 runs it against an open-addressing set in shared
+// memory (membership is all that matters for the output, so any exact set
+// gives numpy's bits) and then the shuffle; the warp clears the set and
+// gathers the picked lengths.  The tail-shuffle branch (pop > 10000 and
+// need > pop/50) needs a population-sized array and stays on the host.
+constexpr int kMaxStrataDraw = 16;
+struct McDrawParams {
+  const int32_t* lens;  // pool lengths, strata concatenated (device)
+  int32_t* out;         // [ntrials][per_trial]
+  uint64_t seed;
+  int64_t first_trial, ntrials, per_trial;
+  int nstrata;
+  int64_t off[kMaxStrataDraw], pop[kMaxStrataDraw], need[kMaxStrataDraw];
+  int bits[kMaxStrataDraw];  // log2 of the set size per stratum
+  int set_cap, pick_cap;     // shared-memory words for the set and the picks
+};
+
+__global__ void __launch_bounds__(32) k_mc_draw(const __grid_constant__ McDrawParams q) {
+  extern __shared__ uint32_t sm[];
+  uint32_t* set = sm;                // [set_cap]
+  uint32_t* picks = sm + q.set_cap;  // [pick_cap]
+  const int lane = threadIdx.x;
+  constexpr uint32_t kEmpty = 0xffffffffu;
+  for (int64_t tr = blockIdx.x; tr < q.ntrials; tr += gridDim.x) {
+    const uint64_t key = (uint64_t)(q.first_trial + tr);
+    rng::Pcg64 g(rng::SeedSeq(q.seed, &key, 1));  // used by lane 0 only
+    int64_t row = 0;
+    for (int k = 0; k < q.nstrata; ++k) {
+      const int64_t need = q.need[k];
+      if (need == 0) continue;
+      const int bits = q.bits[k];
+      const uint32_t hmask = (1u << bits) - 1u;
+      for (int i = lane; i <= (int)hmask; i += 32) set[i] = kEmpty;
+      __syncwarp();
+      if (lane == 0) {
+        const int64_t pop = q.pop[k];
+        for (int64_t j = pop - need; j < pop; ++j) {  // Floyd (numpy _generator choice)
+          const uint32_t val = (uint32_t)g.bounded((uint64_t)j);
+          uint32_t h = (val * 2654435761u) >> (32 - bits);
+          while (set[h] != kEmpty && set[h] != val) h = (h + 1) & hmask;
+          uint32_t pick = val;
+          if (set[h] == kEmpty) {
+            set[h] = val;
+          } else {  // val already drawn: take j itself (never in the set yet)
+            pick = (uint32_t)j;
+            uint32_t h2 = ((uint32_t)j * 2654435761u) >> (32 - bits);
+            while (set[h2] != kEmpty) h2 = (h2 + 1) & hmask;
+            set[h2] = pick;
+          }
+          picks[j - pop + need] = pick;
+        }
+        for (int64_t i = need - 1; i >= 1; --i) {  // _shuffle_int(size, 1, idx)
+          const int64_t j = (int64_t)g.bounded((uint64_t)i);
+          const uint32_t t0 = picks[j];
+          picks[j] = picks[i];
+          picks[i] = t0;
+        }
+      }
+      __syncwarp();
+      int32_t* o = q.out + tr * q.per_trial + row;
+      const int32_t* L = q.lens + q.off[k];
+      for (int64_t i = lane; i < need; i += 32) o[i] = L[picks[i]];
+      __syncwarp();
+      row += need;
+    }
+  }
+}
+
 }  // namespace
 }  // namespace b2
 
 using namespace b2;
+
+extern "C" int b2_mc_draw_device(const int32_t* pool_lens, const int64_t* pool_sizes, int nstrata,
+                                 const int64_t* counts, int num_gpus, uint64_t seed, int64_t first_trial,
+                                 int64_t ntrials, int32_t* out, void* stream) {
+  B2_REQUIRE(pool_lens && pool_sizes && counts && out, B2_ERR_INVALID, "NULL argument");
+  B2_REQUIRE(nstrata >= 1 && nstrata <= kMaxStrataDraw, B2_ERR_UNSUPPORTED, "nstrata must be in [1, %d]",
+             kMaxStrataDraw);
+  B2_REQUIRE(num_gpus >= 1 && ntrials >= 0 && first_trial >= 0, B2_ERR_INVALID, "bad shape");
+  McDrawParams q{};
+  q.lens = pool_lens;
+  q.out = out;
+  q.seed = seed;
+  q.first_trial = first_trial;
+  q.ntrials = ntrials;
+  q.nstrata = nstrata;
+  int64_t off = 0, per = 0, maxneed = 0;
+  int maxbits = 5;
+  for (int k = 0; k < nstrata; ++k) {
+    const int64_t need = counts[k] * (int64_t)num_gpus, pop = pool_sizes[k];
+    B2_REQUIRE(counts[k] >= 0 && need <= pop, B2_ERR_INVALID,
+               "corpus exhausted within a trial: a stratum holds %lld samples but the trial needs %lld",
+               (long long)pop, (long long)need);
+    B2_REQUIRE(pop < (int64_t)0xffffffffll, B2_ERR_UNSUPPORTED, "stratum %d too large for device draws", k);
+    B2_REQUIRE(!(need > 0 && pop > 10000 && need > pop / 50), B2_ERR_UNSUPPORTED,
+               "stratum %d uses numpy's tail-shuffle branch (host draws only)", k);
+    int bits = 5;  // set of >= need / 0.75 slots, power of two
+    while ((int64_t)(1ll << bits) * 3 < need * 4) ++bits;
+    q.off[k] = off;
+    q.pop[k] = pop;
+    q.need[k] = need;
+    q.bits[k] = bits;
+    off += pop;
+    per += need;
+    maxneed = std::max(maxneed, need);
+    maxbits = std::max(maxbits, bits);
+  }
+  q.per_trial = per;
+  q.set_cap = 1 << maxbits;
+  q.pick_cap = (int)std::max<int64_t>(1, maxneed);
+  const size_t smem = sizeof(uint32_t) * ((size_t)q.set_cap + q.pick_cap);
+  B2_REQUIRE(smem <= 200 * 1024, B2_ERR_UNSUPPORTED, "trial too large for device draws (%zu B of shared memory)", smem);
+  if (ntrials == 0) return B2_OK;
+  B2_CHECK(cudaFuncSetAttribute(k_mc_draw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  B2_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mc_draw, 32, smem));
+  B2_REQUIRE(occ >= 1, B2_ERR_UNSUPPORTED, "device draw kernel cannot be resident");
+  const DeviceInfo& di = device_info();
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntrials, (int64_t)di.sm_count * occ));
+  k_mc_draw<<<grid, 32, smem, (cudaStream_t)stream>>>(q);
+  B2_CHECK(cudaGetLastError());
+  return B2_OK;
+}
 
 extern "C" int b2_mc_token_counts(const int32_t* mat, int64_t ntrials, int b, int num_gpus, int gpus_per_node,
                                   int strategy, int scan, int32_t max_len, int64_t* counts, int64_t* mins,

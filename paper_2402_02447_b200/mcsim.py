@@ -7,11 +7,13 @@ over trials give the balance table (``run_balance_experiment`` :79-81,
 
 Split by where each piece is cheapest, bit-exact with the reference:
 
-* **draws** (host, C++ threads): ``b2_mc_draw`` ports numpy's
-  ``SeedSequence(seed, spawn_key=(t,))`` -> PCG64 -> ``Generator.choice(
-  replace=False)`` for every trial (``derive_rng``, seeding.py:8-16;
-  ``_stratified_matrix`` :166-180; ``_draw_uniform`` :146-151).  Trials are
-  independent, so they split across threads.
+* **draws** (device, one warp per trial: ``b2_mc_draw_device``; or host C++
+  threads: ``b2_mc_draw``) port numpy's ``SeedSequence(seed, spawn_key=(t,))``
+  -> PCG64 -> ``Generator.choice(replace=False)`` for every trial
+  (``derive_rng``, seeding.py:8-16; ``_stratified_matrix`` :166-180;
+  ``_draw_uniform`` :146-151).  Trials are independent.  The device path
+  covers numpy's Floyd branch (every paper configuration); the tail-shuffle
+  branch (a large share of a pool) stays on the host threads.
 * **token counts** (device): ``b2_mc_token_counts`` sorts each node's pool
   (LOCAL_PRESORT), or the whole batch (GLOBAL_PRESORT), deals raster / snake,
   sums per GPU in int64 and reduces min / max per trial, all trials in one
@@ -19,8 +21,8 @@ Split by where each piece is cheapest, bit-exact with the reference:
 * **aggregation** (host): the reference's own numpy expressions on the
   int64 min / max arrays (:290-306), so the float statistics match bit for bit.
 
-Draw and count overlap chunk by chunk (host threads fill pinned buffer i+1
-while the GPU counts chunk i).  ``PACKING`` needs ``pack_corpus``, which is
+With host draws, draw and count overlap chunk by chunk (host threads fill
+pinned buffer i+1 while the GPU counts chunk i).  ``PACKING`` needs ``pack_corpus``, which is
 outside this build's scope, and raises ``NotImplementedError``.
 """
 
@@ -161,6 +163,27 @@ def draw_trials(exp: BalanceExperiment, first_trial: int, ntrials: int, out: np.
     return out
 
 
+def draw_trials_device(exp: BalanceExperiment, first_trial: int, ntrials: int, out: torch.Tensor | None = None,
+                       prep: _Prepared | None = None, pools: torch.Tensor | None = None, stream=None):
+    """Device draws of trials [first, first+n) into a CUDA int32 [n, b*G] tensor
+    (``b2_mc_draw_device``: the same bits as ``draw_trials``).  Returns None when
+    a stratum falls in numpy's tail-shuffle branch (host draws only)."""
+    prep = prep if prep is not None else _prepare(exp)
+    lib = _lib.load()
+    G, b = exp.topo.total_gpus, exp.local_batch
+    if pools is None:
+        pools = torch.from_numpy(prep.pools).cuda()
+    if out is None:
+        out = torch.empty((ntrials, b * G), dtype=torch.int32, device="cuda")
+    rc = lib.b2_mc_draw_device(pools.data_ptr(), prep.pool_sizes.ctypes.data, int(prep.pool_sizes.size),
+                               prep.counts.ctypes.data, G, int(exp.seed) & (2**64 - 1), int(first_trial),
+                               int(ntrials), out.data_ptr(), _lib.stream_ptr(stream))
+    if rc == _lib.B2_ERR_UNSUPPORTED:
+        return None
+    _lib.check(rc)
+    return out
+
+
 def trial_token_counts(exp: BalanceExperiment, mat: torch.Tensor, max_len: int, counts: bool = False,
                        stream=None):
     """Device: [n, b*G] int32 length matrices -> (mins, maxs[, counts [n, G]]) int64 on the device."""
@@ -200,10 +223,20 @@ def _stderr(values: np.ndarray) -> float:
     return float(values.std(ddof=1) / math.sqrt(values.size))
 
 
-def run_trials(exp: BalanceExperiment, chunk: int = 4096, threads: int | None = None):
-    """All trials: (mins, maxs) int64 host arrays.  Host draws of chunk i+1
-    overlap the device counts of chunk i (two pinned buffers, one copy stream)."""
+def run_trials(exp: BalanceExperiment, chunk: int = 4096, threads: int | None = None, draws: str = "auto"):
+    """All trials: (mins, maxs) int64 host arrays.
+
+    draws="device" (and "auto" when every stratum is in numpy's Floyd branch):
+    draws and counts both on the GPU, chunk by chunk.  draws="host" (and the
+    "auto" fallback): host-thread draws of chunk i+1 overlap the device
+    counts of chunk i (two pinned buffers, one copy stream)."""
     prep = _prepare(exp)
+    if draws in ("auto", "device"):
+        res = _run_trials_device(exp, prep, chunk)
+        if res is not None:
+            return res
+        if draws == "device":
+            raise _lib.B2Error("device draws unsupported for this experiment (numpy tail-shuffle branch)")
     G, b = exp.topo.total_gpus, exp.local_batch
     T = exp.trials
     chunk = max(1, min(chunk, T))
@@ -225,6 +258,28 @@ def run_trials(exp: BalanceExperiment, chunk: int = 4096, threads: int | None = 
         maxs[t0:t0 + n].copy_(mx, non_blocking=True)
         bads.append(bad)
         done[k].record(stream)
+    if int(torch.stack(bads).max()) != 0:
+        raise ValueError("a drawn length is outside [1, max length] (corrupt corpus)")
+    return mins.cpu().numpy(), maxs.cpu().numpy()
+
+
+def _run_trials_device(exp: BalanceExperiment, prep: _Prepared, chunk: int):
+    G, b = exp.topo.total_gpus, exp.local_batch
+    T = exp.trials
+    chunk = max(1, min(chunk, T))
+    pools = torch.from_numpy(prep.pools).cuda()
+    mat = torch.empty((chunk, b * G), dtype=torch.int32, device="cuda")
+    mins = torch.empty(T, dtype=torch.int64, device="cuda")
+    maxs = torch.empty(T, dtype=torch.int64, device="cuda")
+    bads = []
+    for t0 in range(0, T, chunk):
+        n = min(chunk, T - t0)
+        if draw_trials_device(exp, t0, n, out=mat[:n], prep=prep, pools=pools) is None:
+            return None
+        mn, mx, _, bad = trial_token_counts(exp, mat[:n], prep.max_len)
+        mins[t0:t0 + n].copy_(mn)
+        maxs[t0:t0 + n].copy_(mx)
+        bads.append(bad)
     if int(torch.stack(bads).max()) != 0:
         raise ValueError("a drawn length is outside [1, max length] (corrupt corpus)")
     return mins.cpu().numpy(), maxs.cpu().numpy()

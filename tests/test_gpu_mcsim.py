@@ -70,3 +70,36 @@ def test_mc_engine_paper_scale_vs_oracle(strategy, scan):
         assert cnt[t].tolist() == ref.tolist(), t
     assert np.array_equal(mins.cpu().numpy(), cnt.min(axis=1))
     assert np.array_equal(maxs.cpu().numpy(), cnt.max(axis=1))
+
+
+@pytest.mark.parametrize("case", range(len(GOLDEN["cases"])))
+def test_device_draws_equal_host_draws(case):
+    """b2_mc_draw_device (one warp per trial) == b2_mc_draw (host threads) == numpy, bit for bit."""
+    from paper_2402_02447_b200.mcsim import draw_trials_device
+
+    c = GOLDEN["cases"][case]
+    lengths = O.generate_lengths(GOLDEN["corpus_n"], GOLDEN["corpus_seed"])
+    exp = _exp(c, lengths)
+    prep = _prepare(exp)
+    host = draw_trials(exp, 5, 30, prep=prep)
+    dev = draw_trials_device(exp, 5, 30, prep=prep)
+    assert dev is not None
+    assert np.array_equal(dev.cpu().numpy(), host)
+
+
+def test_device_draws_paper_scale_and_tail_shuffle_fallback():
+    from paper_2402_02447_b200.mcsim import draw_trials_device, run_trials
+
+    lengths = O.generate_lengths(10_000_000, 2402)
+    for strategy in ("local_presort", "none"):
+        exp = BalanceExperiment(strategy, Topology(128, 8), lengths, seed=4, local_batch=16, trials=40)
+        prep = _prepare(exp)
+        dev = draw_trials_device(exp, 0, 40, prep=prep)
+        assert np.array_equal(dev.cpu().numpy(), draw_trials(exp, 0, 40, prep=prep))
+    # 20,000-sample corpus, 32 GPUs x lb 16 = 512 > 20,000 // 50: numpy's tail-shuffle branch
+    small = O.generate_lengths(20_000, 606)
+    exp = BalanceExperiment("none", Topology(4, 8), small, seed=8, local_batch=16, trials=25)
+    assert draw_trials_device(exp, 0, 25) is None
+    mins, maxs = run_trials(exp)  # auto: falls back to host draws
+    ref = [O.mcsim_trial_counts("none", small, O.DEFAULT_BOUNDS, 16, 4, 8, False, 8, t) for t in range(25)]
+    assert mins.tolist() == [int(r.min()) for r in ref] and maxs.tolist() == [int(r.max()) for r in ref]

@@ -27,7 +27,7 @@ def header_symbols():
 def test_library_exports_header_symbols():
     lib = _lib.load(require_device=False)
     syms = header_symbols()
-    assert len(syms) == 29, syms
+    assert len(syms) == 30, syms
     for s in syms:
         assert hasattr(lib, s), s
         assert s in _lib.SIGNATURES, s
