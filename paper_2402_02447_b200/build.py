@@ -27,7 +27,7 @@ def nvcc() -> str:
 
 def build(verbose: bool = False) -> Path:
     srcs = [PKG / "csrc" / s for s in SOURCES]
-    deps = srcs + list((PKG / "csrc").glob("*.cuh")) + [ROOT / "include" / "b2ddp.h"]
+    deps = srcs + list((PKG / "csrc").glob("*.cuh")) + list((PKG / "csrc").glob("*.h")) + [ROOT / "include" / "b2ddp.h"]
     if OUT.exists() and all(OUT.stat().st_mtime >= d.stat().st_mtime for d in deps):
         return OUT
     OUT.parent.mkdir(parents=True, exist_ok=True)
