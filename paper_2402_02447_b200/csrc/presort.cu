@@ -21,6 +21,8 @@
 #include <cub/block/block_radix_sort.cuh>
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 #include <type_traits>
 
 namespace b2 {
@@ -159,6 +161,126 @@ __global__ void __launch_bounds__(32 * WARPS) k_presort_deal_warp(const __grid_c
   }
 }
 
+// Warp-per-pool COUNTING sort (lengths are small integers): histogram of the
+// pool's lengths in shared memory (the atomic's return value ranks each key
+// inside its bin), one warp scan over the bins, a scatter into sorted order,
+// then ids ordered inside each multi-key bin (equal lengths; a handful of
+// keys on real data).  O(pool) work instead of the bitonic network's
+// O(pool log^2 pool) 64-bit compare-exchanges; (-len, id) is unique per
+// sample, so the output is the same.  Pools <= 512 keys, lengths <= 1024.
+constexpr int kCntBins = 1024;
+constexpr int kCntMaxSeg = 512;
+
+template <int WARPS>
+__global__ void __launch_bounds__(32 * WARPS) k_presort_deal_count(const __grid_constant__ PresortParams p) {
+  __shared__ int s_hist[WARPS][kCntBins];         // counts, then bin starts
+  __shared__ int32_t s_sid[WARPS][kCntMaxSeg];    // sorted ids
+  __shared__ int16_t s_slen[WARPS][kCntMaxSeg];   // sorted lengths
+  __shared__ int32_t s_oid[WARPS][kCntMaxSeg];    // dealt [lane][row]
+  __shared__ int16_t s_olen[WARPS][kCntMaxSeg];
+  constexpr int KM = kCntMaxSeg / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int M = p.max_len, P = p.seg_len;
+  const int per = (M + 31) / 32;  // bins per lane in the scan
+  int* hist = s_hist[w];
+  const int64_t nwarps = (int64_t)gridDim.x * WARPS;
+  for (int64_t seg = (int64_t)blockIdx.x * WARPS + w; seg < p.nseg; seg += nwarps) {
+    const int64_t base = seg * P;
+    for (int b = lane; b < M; b += 32) hist[b] = 0;
+    __syncwarp();
+    int32_t id[KM];
+    int16_t len[KM], rk[KM];
+    long long first_bad = -1;
+#pragma unroll
+    for (int j = 0; j < KM; ++j) {
+      const int i = j * 32 + lane;  // striped: coalesced loads
+      if (i < P) {
+        int32_t L = p.lens[base + i];
+        const int32_t D = p.ids[base + i];
+        if (!(L >= 1 && L <= M && D >= 0 && D <= p.max_id)) {
+          if (first_bad < 0) first_bad = base + i;
+          L = L < 1 ? 1 : (L > M ? M : L);  // keep the slot well-formed; the caller raises
+        }
+        id[j] = D;
+        len[j] = (int16_t)L;
+        rk[j] = (int16_t)atomicAdd(&hist[M - L], 1);  // bin 0 = longest
+      }
+    }
+    if (first_bad >= 0 && p.bad) atomicMin(reinterpret_cast<unsigned long long*>(p.bad), (unsigned long long)first_bad);
+    __syncwarp();
+    {  // exclusive scan over the M bins: `per` contiguous bins per lane
+      const int b0 = lane * per, b1 = min(b0 + per, M);
+      int sum = 0;
+      for (int b = b0; b < b1; ++b) sum += hist[b];
+      int inc = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      int ex = inc - sum;
+      for (int b = b0; b < b1; ++b) {
+        const int c = hist[b];
+        hist[b] = ex;
+        ex += c;
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < KM; ++j) {
+      const int i = j * 32 + lane;
+      if (i < P) {
+        const int pos = hist[M - len[j]] + rk[j];
+        s_sid[w][pos] = id[j];
+        s_slen[w][pos] = len[j];
+      }
+    }
+    __syncwarp();
+    {  // equal lengths: ids ascending inside each bin (insertion sort; bins are tiny)
+      const int b0 = lane * per, b1 = min(b0 + per, M);
+      for (int b = b0; b < b1; ++b) {
+        const int st = hist[b], en = b + 1 < M ? hist[b + 1] : P;
+        for (int x = st + 1; x < en; ++x) {
+          const int32_t v = s_sid[w][x];
+          int y = x - 1;
+          while (y >= st && s_sid[w][y] > v) {
+            s_sid[w][y + 1] = s_sid[w][y];
+            --y;
+          }
+          s_sid[w][y + 1] = v;
+        }
+      }
+    }
+    __syncwarp();
+    for (int q = lane; q < P; q += 32) {  // deal (balance.py:59-70)
+      const int r = q / p.lanes, c = q - r * p.lanes;
+      const int ln = (p.snake && (r & 1)) ? p.lanes - 1 - c : c;
+      s_oid[w][ln * p.rows + r] = s_sid[w][q];
+      s_olen[w][ln * p.rows + r] = s_slen[w][q];
+    }
+    __syncwarp();
+    int32_t* out = p.out_ids + base;
+    for (int i = lane; i < P; i += 32) out[i] = s_oid[w][i];
+    if (p.tokens)
+      for (int l = lane; l < p.lanes; l += 32) {
+        int64_t sum = 0;  // per-lane token sum (_from_per_gpu, balance.py:54-56)
+        for (int r = 0; r < p.rows; ++r) sum += s_olen[w][l * p.rows + r];
+        p.tokens[seg * p.lanes + l] = sum;
+      }
+    __syncwarp();
+  }
+}
+
+template <int WARPS>
+int launch_count(const PresortParams& p, cudaStream_t st) {
+  const DeviceInfo& di = device_info();
+  const int64_t blocks = (p.nseg + WARPS - 1) / WARPS;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)di.sm_count * 16));
+  k_presort_deal_count<WARPS><<<grid, 32 * WARPS, 0, st>>>(p);
+  B2_CHECK(cudaGetLastError());
+  return B2_OK;
+}
+
 template <int K, int WARPS>
 int launch_warp(const PresortParams& p, cudaStream_t st) {
   const DeviceInfo& di = device_info();
@@ -221,6 +343,16 @@ extern "C" int b2_presort_deal(const int32_t* ids, const int32_t* lens, int64_t 
   p.tokens = tokens;
   p.bad = bad;
   B2_REQUIRE(p.end_bit <= 64, B2_ERR_UNSUPPORTED, "key does not fit 64 bits");
+  static int variant = -1;  // B2_PRESORT_PATH=bitonic forces the network (A/B runs, tests)
+  if (variant < 0) {
+    const char* e = getenv("B2_PRESORT_PATH");
+    variant = (e && !strcmp(e, "bitonic")) ? 1 : 0;
+  }
+  // counting sort pays when the pool fills at least half of the length bins
+  // (lb48: 384 keys / 512 bins, 1.37x over the network); smaller pools sort
+  // faster in registers than the bins can be cleared and scanned (lb16: 3x)
+  if (!out_pos && variant == 0 && seg_len <= kCntMaxSeg && max_len <= kCntBins && 2 * seg_len >= max_len)
+    return launch_count<4>(p, st);
   if (!out_pos) {  // no input slots needed: warp-per-pool bitonic network
     if (seg_len <= 64) return launch_warp<2, 8>(p, st);
     if (seg_len <= 128) return launch_warp<4, 8>(p, st);

@@ -299,3 +299,25 @@ def test_h2_pipeline_end_to_end_full_config():
         ref_gpu, ref_tok = O.assign_local_presort(per_gpu_ids, per_gpu_lens, 1, 8, True)
         assert out[t].tolist() == ref_gpu, t
         assert tok[t].tolist() == list(ref_tok), t
+
+
+@pytest.mark.parametrize("lenrange", [(1, 4), (1, 40), (1, 192), (180, 192)])
+@pytest.mark.parametrize("seg_len,lanes", [(128, 8), (384, 8), (512, 4), (96, 3)])
+def test_presort_paths_agree_with_heavy_ties(lenrange, seg_len, lanes):
+    """Counting-sort path (max_len <= min(1024, 2 pool)), bitonic path (max_len > 1024) and
+    the stable radix path (with_pos) give the oracle's deal, with many equal
+    lengths (ties broken by id) and ragged pools."""
+    rng = np.random.default_rng(seg_len * 7 + lenrange[1])
+    nseg = 300
+    ids = np.stack([rng.permutation(10 * seg_len)[:seg_len] for _ in range(nseg)]).astype(np.int32)
+    lens = rng.integers(lenrange[0], lenrange[1] + 1, size=(nseg, seg_len)).astype(np.int32)
+    di, dl = torch.from_numpy(ids.reshape(-1)).cuda(), torch.from_numpy(lens.reshape(-1)).cuda()
+    outs = []
+    for max_len, pos in ((2 * seg_len, False), (4096, False), (512, True)):
+        r = presort_deal(di, dl, seg_len, lanes, "snake", max_len=max_len, max_id=10 * seg_len, with_pos=pos)
+        outs.append((r[0].cpu().numpy(), r[1].cpu().numpy()))
+    for o, t in outs[1:]:
+        assert np.array_equal(o, outs[0][0]) and np.array_equal(t, outs[0][1])
+    ro, rt = O.presort_deal_segments(ids.reshape(-1), lens.reshape(-1), seg_len, lanes, True)
+    np.testing.assert_array_equal(outs[0][0], ro)
+    np.testing.assert_array_equal(outs[0][1], rt)
