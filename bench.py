@@ -332,6 +332,15 @@ def bench_clip(args, rank, world, local):
                          "comm_dtype": "bf16",
                          "collective": (f"fused in K4 ({fsync.transport})" if launches_per_step == 1
                                         else "ncclAllReduce avg per 25 MiB bucket, side stream")}
+        # roofline of the fused step (B200_PROFILING.md): bytes that must cross NVLink per
+        # direction per GPU / the measured 770 GB/s peer copy; two-shot P2P moves 2(N-1)/N of
+        # the bf16 gradient each way, NVLS one full copy
+        per_dir = dim * 2 * (2 * (world - 1) / world if getattr(fsync, "mc", 0) == 0 else 1.0) \
+            if launches_per_step == 1 else dim * 2 * 2 * (world - 1) / world
+        res["nvlink"]["roofline"] = {
+            "bound": "nvlink", "bytes_per_dir_per_gpu": per_dir, "achieved": per_dir / (ms * 1e-3) / 1e9,
+            "peak": 770.0, "peak_src": "measured peer copy per direction (B200_PROFILING.md)", "unit": "GB/s",
+            "frac": per_dir / (ms * 1e-3) / 1e9 / 770.0, "floor_ms": per_dir / 770e9 * 1e3}
 
     # e2e: pinned host fp32 gradients -> device -> sync -> host result, through the public API
     host = torch.empty((1, dim), dtype=torch.float32, pin_memory=True)
