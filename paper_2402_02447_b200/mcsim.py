@@ -32,14 +32,13 @@ import math
 import os
 from dataclasses import dataclass, replace
 from enum import Enum
-from typing import Sequence
 
 import numpy as np
 import torch
 
 from . import _lib
 from .balance import ScanPattern
-from .seqdata import MAX_SEQ_LEN, Sample, Topology
+from .seqdata import MAX_SEQ_LEN, Topology
 from .strata import DEFAULT_STRATUM_BOUNDARIES, allocate_counts, derive_seed, stratify_lengths
 
 _STRATEGY_CODE = {"none": 0, "stratified": 1, "local_presort": 2, "global_presort": 3}

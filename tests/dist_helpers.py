@@ -35,11 +35,9 @@ def oracle_clip(grad, out, segments, limit, post_scale=1.0, norms=None, coefs=No
 
     for i, (a, o, n) in enumerate(segments):
         g = grad[a:a + n].double().numpy()
-        nrm = float(np.linalg.norm(g))
-        cf = (limit / nrm) if nrm >= limit else 1.0
-        out[o:o + n] = torch.from_numpy(g * cf * post_scale).to(out.dtype)
+        out[o:o + n] = torch.from_numpy(O.clip_by_norm(g, limit) * post_scale).to(out.dtype)
         if norms is not None:
-            norms[i] = nrm
+            norms[i] = float(np.linalg.norm(g))
 
 
 def worker_grad(rank: int, dim: int) -> torch.Tensor:

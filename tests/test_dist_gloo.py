@@ -8,7 +8,6 @@ one allreduce per bucket averages them, in reverse bucket order
 """
 
 import numpy as np
-import pytest
 import torch
 import torch.multiprocessing as mp
 
