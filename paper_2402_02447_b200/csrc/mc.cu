@@ -191,9 +191,12 @@ struct McDrawParams {
 };
 
 __global__ void __launch_bounds__(32) k_mc_draw(const __grid_constant__ McDrawParams q) {
+  // one shared region per trial: the Floyd set, then (reloaded) the picks for
+  // the shuffle; during Floyd the picks go straight to the trial's output
+  // rows in global memory (fire-and-forget stores, off the critical path)
   extern __shared__ uint32_t sm[];
-  uint32_t* set = sm;                // [set_cap]
-  uint32_t* picks = sm + q.set_cap;  // [pick_cap]
+  uint32_t* set = sm;    // [set_cap] during Floyd
+  uint32_t* picks = sm;  // [need] during the shuffle
   const int lane = threadIdx.x;
   constexpr uint32_t kEmpty = 0xffffffffu;
   for (int64_t tr = blockIdx.x; tr < q.ntrials; tr += gridDim.x) {
@@ -207,6 +210,7 @@ __global__ void __launch_bounds__(32) k_mc_draw(const __grid_constant__ McDrawPa
       const uint32_t hmask = (1u << bits) - 1u;
       for (int i = lane; i <= (int)hmask; i += 32) set[i] = kEmpty;
       __syncwarp();
+      int32_t* o = q.out + tr * q.per_trial + row;  // this stratum's output rows (scratch first)
       if (lane == 0) {
         const int64_t pop = q.pop[k];
         for (int64_t j = pop - need; j < pop; ++j) {  // Floyd (numpy _generator choice)
@@ -222,8 +226,13 @@ __global__ void __launch_bounds__(32) k_mc_draw(const __grid_constant__ McDrawPa
             while (set[h2] != kEmpty) h2 = (h2 + 1) & hmask;
             set[h2] = pick;
           }
-          picks[j - pop + need] = pick;
+          o[j - pop + need] = (int32_t)pick;
         }
+      }
+      __syncwarp();  // orders lane 0's global stores before the warp's reload
+      for (int64_t i = lane; i < need; i += 32) picks[i] = (uint32_t)o[i];
+      __syncwarp();
+      if (lane == 0) {
         for (int64_t i = need - 1; i >= 1; --i) {  // _shuffle_int(size, 1, idx)
           const int64_t j = (int64_t)g.bounded((uint64_t)i);
           const uint32_t t0 = picks[j];
@@ -232,7 +241,6 @@ __global__ void __launch_bounds__(32) k_mc_draw(const __grid_constant__ McDrawPa
         }
       }
       __syncwarp();
-      int32_t* o = q.out + tr * q.per_trial + row;
       const int32_t* L = q.lens + q.off[k];
       for (int64_t i = lane; i < need; i += 32) o[i] = L[picks[i]];
       __syncwarp();
@@ -284,7 +292,7 @@ extern "C" int b2_mc_draw_device(const int32_t* pool_lens, const int64_t* pool_s
   q.per_trial = per;
   q.set_cap = 1 << maxbits;
   q.pick_cap = (int)std::max<int64_t>(1, maxneed);
-  const size_t smem = sizeof(uint32_t) * ((size_t)q.set_cap + q.pick_cap);
+  const size_t smem = sizeof(uint32_t) * (size_t)std::max<int64_t>(q.set_cap, q.pick_cap);
   B2_REQUIRE(smem <= 200 * 1024, B2_ERR_UNSUPPORTED, "trial too large for device draws (%zu B of shared memory)", smem);
   if (ntrials == 0) return B2_OK;
   B2_CHECK(cudaFuncSetAttribute(k_mc_draw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
