@@ -590,7 +590,7 @@ def bench_mcsim(args, lens):
     mat = draw_trials(exp, 0, n_d, prep=prep, threads=threads)
     t_draw = time.perf_counter() - t0
     # device draws alone (one warp per trial, CUDA events)
-    pools = torch.from_numpy(prep.pools).cuda()
+    pools = prep.pools_dev
     dmat = torch.empty((n_d, keys_per_trial), dtype=torch.int32, device="cuda")
     draw_trials_device(exp, 0, n_d, out=dmat, prep=prep, pools=pools)
     torch.cuda.synchronize()

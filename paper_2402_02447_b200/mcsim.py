@@ -107,10 +107,18 @@ def _lengths_of(samples) -> np.ndarray:
 
 @dataclass
 class _Prepared:
-    pools: np.ndarray        # int32 lengths of the draw pools, concatenated
+    pools_dev: torch.Tensor  # int32 lengths of the draw pools, concatenated (device)
     pool_sizes: np.ndarray   # int64 per pool
     counts: np.ndarray       # int64 per-GPU draws per pool
     max_len: int
+    _pools_host: np.ndarray | None = None
+
+    @property
+    def pools(self) -> np.ndarray:
+        """Host copy of the pools (for the host draw threads), made on first use."""
+        if self._pools_host is None:
+            self._pools_host = np.ascontiguousarray(self.pools_dev.cpu().numpy())
+        return self._pools_host
 
 
 def _prepare(exp: BalanceExperiment) -> _Prepared:
@@ -119,10 +127,15 @@ def _prepare(exp: BalanceExperiment) -> _Prepared:
         raise NotImplementedError("the PACKING strategy needs pack_corpus, outside this build's scope (SURVEY §2)")
     lengths = _lengths_of(exp.samples)
     G, b = exp.topo.total_gpus, exp.local_batch
+    if lengths.min() < 1:
+        raise ValueError(f"sample length must be >= 1, got {int(lengths.min())}")
+    uniform = exp.strategy in (Strategy.NONE, Strategy.GLOBAL_PRESORT)
+    if uniform and b * G > lengths.size:  # _draw_uniform :147-150
+        raise ValueError(f"corpus exhausted within a trial: needs {b * G} samples, corpus has {lengths.size}")
+    lens_dev = torch.from_numpy(lengths.astype(np.int32)).cuda()
     if exp.strategy in (Strategy.STRATIFIED, Strategy.LOCAL_PRESORT):
-        ds = stratify_lengths(lengths, exp.stratum_boundaries)  # K2, stable per stratum (strata.py:61-83)
-        ids = ds.ids.cpu().numpy()
-        pools = lengths[ids].astype(np.int32)
+        ds = stratify_lengths(lens_dev, exp.stratum_boundaries)  # K2, stable per stratum (strata.py:61-83)
+        pools = lens_dev[ds.ids.long()]  # the strata's lengths, stratum after stratum (device gather)
         sizes = np.asarray(ds.counts, dtype=np.int64)
         counts = np.asarray(allocate_counts(ds.probs, b).counts, dtype=np.int64)
         for c, n in zip(counts, sizes):  # _stratified_matrix :170-177
@@ -133,17 +146,10 @@ def _prepare(exp: BalanceExperiment) -> _Prepared:
                     f"samples but the trial needs {need}"
                 )
     else:
-        pools = lengths.astype(np.int32)
+        pools = lens_dev
         sizes = np.asarray([lengths.size], dtype=np.int64)
         counts = np.asarray([b], dtype=np.int64)
-        if b * G > lengths.size:  # _draw_uniform :147-150
-            raise ValueError(
-                f"corpus exhausted within a trial: needs {b * G} samples, corpus has {lengths.size}"
-            )
-        if lengths.min() < 1:
-            raise ValueError(f"sample length must be >= 1, got {int(lengths.min())}")
-    return _Prepared(pools=np.ascontiguousarray(pools), pool_sizes=sizes, counts=counts,
-                     max_len=int(lengths.max()))
+    return _Prepared(pools_dev=pools.contiguous(), pool_sizes=sizes, counts=counts, max_len=int(lengths.max()))
 
 
 def draw_trials(exp: BalanceExperiment, first_trial: int, ntrials: int, out: np.ndarray | torch.Tensor | None = None,
@@ -171,7 +177,7 @@ def draw_trials_device(exp: BalanceExperiment, first_trial: int, ntrials: int, o
     lib = _lib.load()
     G, b = exp.topo.total_gpus, exp.local_batch
     if pools is None:
-        pools = torch.from_numpy(prep.pools).cuda()
+        pools = prep.pools_dev
     if out is None:
         out = torch.empty((ntrials, b * G), dtype=torch.int32, device="cuda")
     rc = lib.b2_mc_draw_device(pools.data_ptr(), prep.pool_sizes.ctypes.data, int(prep.pool_sizes.size),
@@ -266,7 +272,7 @@ def _run_trials_device(exp: BalanceExperiment, prep: _Prepared, chunk: int):
     G, b = exp.topo.total_gpus, exp.local_batch
     T = exp.trials
     chunk = max(1, min(chunk, T))
-    pools = torch.from_numpy(prep.pools).cuda()
+    pools = prep.pools_dev
     mat = torch.empty((chunk, b * G), dtype=torch.int32, device="cuda")
     mins = torch.empty(T, dtype=torch.int64, device="cuda")
     maxs = torch.empty(T, dtype=torch.int64, device="cuda")
