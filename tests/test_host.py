@@ -156,3 +156,33 @@ def test_timeline_model_restatement_matches_reference_golden():
         for mode, total in c["total"].items():
             got = tc.schedule_total(c["t_comp"], c["t_comm"], c["t_clip"], c["t_gclip"], c["t_nred"], mode)
             assert got == total, (mode, got, total)
+
+
+def test_acceptance_criteria_07_08_timeline():
+    """test_acceptance.py:149-165 on the restated model: bucket-wise <= before,
+    bucket-wise - after <= the clip costs, over random plans; and the
+    hand-scheduled B=2 pipeline."""
+    import importlib.util
+    from pathlib import Path
+
+    import numpy as np
+
+    spec = importlib.util.spec_from_file_location(
+        "tc", Path(__file__).resolve().parent.parent / "tools" / "timeline_calibrate.py")
+    tc = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(tc)
+    rng = np.random.default_rng(7)
+    for _ in range(500):
+        B = int(rng.integers(1, 13))
+        comp = rng.uniform(0.0, 5.0, B) * (rng.random(B) < 0.9)
+        comm = rng.uniform(0.0, 5.0, B) * (rng.random(B) < 0.9)
+        if comm.sum() == 0.0:
+            comm[int(rng.integers(B))] = rng.uniform(0.1, 5.0)
+        clip = rng.uniform(0.0, 0.6, B) * (rng.random(B) < 0.8)
+        args = (list(comp), list(comm), list(clip), float(clip.sum()), float(rng.uniform(0.0, 1.0)))
+        bw = tc.schedule_total(*args, "bucket_wise")
+        assert bw <= tc.schedule_total(*args, "before_allreduce") + 1e-9
+        assert bw - tc.schedule_total(*args, "after_allreduce") <= clip.sum() + args[3] + 1e-9
+    # criterion 8 (test_acceptance.py:161-165): B=2, comp [2, 2], comm [3, 3]
+    assert tc.schedule_total([2, 2], [3, 3], [0, 0], 0.0, 0.0, "after_allreduce") == 8.0
+    assert tc.schedule_total([2, 2], [3, 3], [0, 0], 0.0, 0.0, "before_allreduce") == 10.0
