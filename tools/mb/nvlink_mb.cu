@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <vector>
 #include <cstdlib>
+#include <algorithm>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); exit(1); } } while (0)
 
@@ -151,6 +152,61 @@ __global__ void k_pull_tma(const char* __restrict__ peer, int64_t bytes, uint32_
   if (a == 0x12345678u) sink[threadIdx.x] = a;
 }
 
+// two-shot by PUSH only: phase 1 writes my copy of the peer-owned slice into
+// the peer's receive buffer; phase 2 (after both phase 1s) reduces my slice
+// from local memory (stage + recv) and writes the result locally and into
+// the peer's stage.  Every NVLink byte is a remote store.
+template <int U>
+__global__ void k_push_p1(const uint4* __restrict__ mine, uint4* __restrict__ peer_recv, int64_t nv) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv; i += stride * U) {
+    uint4 x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = i + u * stride;
+      if (j < nv) x[u] = __ldcg(mine + j);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = i + u * stride;
+      if (j < nv) __stcg(peer_recv + j, x[u]);
+    }
+  }
+}
+template <int U>
+__global__ void k_push_p2(uint4* __restrict__ stage, const uint4* __restrict__ recv, uint4* __restrict__ peer_stage,
+                          int64_t nv) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv; i += stride * U) {
+    uint4 a[U], b[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = i + u * stride;
+      if (j < nv) {
+        a[u] = __ldcg(stage + j);
+        b[u] = __ldcg(recv + j);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = i + u * stride;
+      if (j < nv) {
+        const __nv_bfloat162* ha = reinterpret_cast<const __nv_bfloat162*>(&a[u]);
+        const __nv_bfloat162* hb = reinterpret_cast<const __nv_bfloat162*>(&b[u]);
+        uint4 y;
+        __nv_bfloat162* hy = reinterpret_cast<__nv_bfloat162*>(&y);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 fa = __bfloat1622float2(ha[k]), fb = __bfloat1622float2(hb[k]);
+          hy[k] = __floats2bfloat162_rn((fa.x + fb.x) * 0.5f, (fa.y + fb.y) * 0.5f);
+        }
+        __stcg(stage + j, y);
+        __stcg(peer_stage + j, y);
+      }
+    }
+  }
+}
+
 struct Dev {
   int id;
   cudaStream_t st;
@@ -236,6 +292,62 @@ int main() {
     }
   }
   if (getenv("MB_ONLY_ASYNC")) return 0;
+  if (getenv("MB_ONLY_PUSH2")) {
+    // buffers: buf = [slice 0 | slice 1] stage (2 x S), recv = S per GPU
+    uint4* recv[2];
+    for (int g = 0; g < 2; ++g) { CK(cudaSetDevice(g)); CK(cudaMalloc(&recv[g], S)); }
+    cudaEvent_t p1[2];
+    for (int g = 0; g < 2; ++g) { CK(cudaSetDevice(g)); CK(cudaEventCreateWithFlags(&p1[g], cudaEventDisableTiming)); }
+    for (int bps : {1, 2}) for (int t : {256, 512}) {
+      const int grid = 148 * bps;
+      float ms = run(d, iters, [&](int g) {
+        // GPU g owns slice g; it pushes its copy of slice (1-g) to the peer's recv
+        k_push_p1<4><<<grid, t, 0, d[g].st>>>(d[g].buf + (1 - g) * nv, recv[1 - g], nv);
+        CK(cudaEventRecord(p1[g], d[g].st));
+        CK(cudaSetDevice(1 - g));
+        CK(cudaSetDevice(g));
+      });
+      (void)ms;
+      // phase-separated timing: p1 on both, cross wait, p2 on both
+      auto iter = [&]() {
+        for (int g = 0; g < 2; ++g) {
+          CK(cudaSetDevice(g));
+          k_push_p1<4><<<grid, t, 0, d[g].st>>>(d[g].buf + (1 - g) * nv, recv[1 - g], nv);
+          CK(cudaEventRecord(p1[g], d[g].st));
+        }
+        for (int g = 0; g < 2; ++g) { CK(cudaSetDevice(g)); CK(cudaStreamWaitEvent(d[g].st, p1[1 - g], 0)); }
+        for (int g = 0; g < 2; ++g) {
+          CK(cudaSetDevice(g));
+          k_push_p2<4><<<grid, t, 0, d[g].st>>>(d[g].buf + g * nv, recv[g], d[1 - g].buf + g * nv, nv);
+        }
+      };
+      float best = 1e30f;
+      for (int rep = 0; rep < 3; ++rep) {
+        for (int g = 0; g < 2; ++g) { CK(cudaSetDevice(g)); CK(cudaDeviceSynchronize()); }
+        CK(cudaSetDevice(0));
+        CK(cudaEventRecord(d[0].e0, d[0].st));
+        for (int k = 0; k < iters; ++k) {
+          iter();
+          for (int g = 0; g < 2; ++g) { CK(cudaSetDevice(g)); CK(cudaEventRecord(d[g].done, d[g].st)); }
+          for (int g = 0; g < 2; ++g) { CK(cudaSetDevice(g)); CK(cudaStreamWaitEvent(d[g].st, d[1 - g].done, 0)); }
+        }
+        CK(cudaSetDevice(0));
+        CK(cudaEventRecord(d[0].e1, d[0].st));
+        CK(cudaEventSynchronize(d[0].e1));
+        float m;
+        CK(cudaEventElapsedTime(&m, d[0].e0, d[0].e1));
+        best = std::min(best, m / iters);
+      }
+      report("2shot_push", 1, bps, t, 4, best, (double)S);
+    }
+    // the pull two-shot for the same sizes, same timing harness
+    for (int bps : {2}) for (int t : {128, 256}) {
+      const int grid = 148 * bps;
+      float ms = run(d, iters, [&](int g) { k_twoshot<4><<<grid, t, 0, d[g].st>>>(d[g].buf + g * nv, d[1 - g].buf + g * nv, nv); });
+      report("2shot_pull", 1, bps, t, 4, ms, (double)S);
+    }
+    return 0;
+  }
   // two-shot: GPU g reduces slice g of the (2 x S) buffer: local slice + the peer's same slice
   SWEEP("2shot", 1, (double)S,
         (k_twoshot<U><<<grid, t, 0, d[g].st>>>(d[g].buf + g * nv, d[1 - g].buf + g * nv, nv)))
