@@ -7,7 +7,8 @@
 // Two launches for ALL rank shards at once (HBM/L2-streaming, 8 B/key
 // algorithmic: 4 B length read, 4 B id written; +4 B if explicit ids are read):
 //   k_strata_count  : one CTA per 4096-key tile -> per-tile per-stratum counts
-//                     (+ the shard's first bad index via atomicMin)
+//                     (striped loads, #{len > bound} per bound, differenced;
+//                     + the shard's first bad index via atomicMin)
 //                     and, in the LAST tile of each shard to finish (atomic
 //                     ticket), the shard's exclusive per-tile prefixes (in
 //                     place over the tile counts) and per-stratum totals —
@@ -78,52 +79,63 @@ struct Packed {
 
 using LoadT = cub::BlockLoad<int32_t, kT, kItems, cub::BLOCK_LOAD_WARP_TRANSPOSE>;
 
-// pass 1: per-tile stratum counts (+ first bad sample of the shard)
+// pass 1: per-tile stratum counts (+ first bad sample of the shard).  Order
+// is irrelevant for counting, so keys load striped (direct coalesced loads),
+// and each thread counts #{len > bound_j} per bound with the bounds in
+// registers; stratum counts are differences of those (stratum 0 also drops
+// lengths < 1; lengths beyond the last bound cancel out).  Bad samples only
+// cost a block OR unless one exists.
 template <int NB>
 __global__ void __launch_bounds__(kT) k_strata_count(const __grid_constant__ StrataParams p) {
-  __shared__ typename LoadT::TempStorage ld;
-  __shared__ int cnt[kMaxStrata];
+  __shared__ int cnt[kMaxStrata + 1];  // [NB] strata, [NB] = valid keys >= 1
   const int tile = blockIdx.x;
   const int g = shard_of_tile(p, tile);
   const int64_t sbeg = p.shard_off[g], send = p.shard_off[g + 1];
   const int64_t lbase = (int64_t)(tile - p.tile_off[g]) * kTile;  // within the shard
   const int valid = (int)min64(kTile, send - sbeg - lbase);
-  if (threadIdx.x < kMaxStrata) cnt[threadIdx.x] = 0;
-  int32_t v[kItems];
-  LoadT(ld).Load(p.len + sbeg + lbase, v, valid, 1);
-  __syncthreads();
-  // per-thread counts packed 16 bits per stratum (<= kItems each), 4 strata per u64
-  constexpr int NW = (NB + 3) / 4;
-  unsigned long long local[NW];
+  if (threadIdx.x <= kMaxStrata) cnt[threadIdx.x] = 0;
+  const int32_t* L = p.len + sbeg + lbase;
+  int32_t bnd[NB];
 #pragma unroll
-  for (int i = 0; i < NW; ++i) local[i] = 0ull;
-  long long first_bad = -1;
+  for (int q = 0; q < NB; ++q) bnd[q] = p.bounds[q];
+  const int32_t blast = p.bounds[p.nb - 1];
+  int32_t v[kItems];
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
-    const int idx = threadIdx.x * kItems + j;
-    if (idx < valid) {
-      const int k = stratum_of<NB>(v[j], p);
-      const bool bad = (k >= p.nb) || (v[j] < 1);
-      if (bad && first_bad < 0) first_bad = lbase + idx;
-      if (!bad) {
-#pragma unroll
-        for (int i = 0; i < NW; ++i)
-          if ((k >> 2) == i) local[i] += 1ull << ((k & 3) * 16);
-      }
-    }
+    const int idx = j * kT + threadIdx.x;
+    v[j] = idx < valid ? L[idx] : 1;  // padding: a length that counts nowhere (fixed below)
   }
-  if (first_bad >= 0) atomicMin(reinterpret_cast<unsigned long long*>(p.bad + g), (unsigned long long)first_bad);
+  int gt[NB];
 #pragma unroll
-  for (int i = 0; i < NW; ++i) {  // warp sums stay < 2^16 per field (32 x 16 keys)
-    unsigned long long s2 = local[i];
+  for (int q = 0; q < NB; ++q) gt[q] = 0;
+  int pos = 0, anybad = 0;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-    if ((threadIdx.x & 31) == 0)
+  for (int j = 0; j < kItems; ++j) {
+    const int32_t x = v[j];
+    pos += (x >= 1);
 #pragma unroll
-      for (int f = 0; f < 4; ++f) {
-        const unsigned c = (unsigned)((s2 >> (16 * f)) & 0xffffull);
-        if (c && 4 * i + f < NB) atomicAdd(&cnt[4 * i + f], (int)c);
-      }
+    for (int q = 0; q < NB; ++q) gt[q] += (x > bnd[q]);
+    anybad |= (x < 1) | (x > blast);
+  }
+  // padding slots were given length 1: they count in `pos` only; remove them
+  pos -= kItems - (valid > threadIdx.x ? (valid - 1 - (int)threadIdx.x) / kT + 1 : 0);
+  __syncthreads();  // cnt zeroed
+  if (__syncthreads_or(anybad)) {  // rare: locate the tile's first bad sample
+    long long first_bad = -1;
+#pragma unroll
+    for (int j = kItems - 1; j >= 0; --j) {  // keeps the smallest index
+      const int idx = j * kT + threadIdx.x;
+      if (idx < valid && (v[j] < 1 || v[j] > blast)) first_bad = lbase + idx;
+    }
+    if (first_bad >= 0) atomicMin(reinterpret_cast<unsigned long long*>(p.bad + g), (unsigned long long)first_bad);
+  }
+  // stratum q < nb: gt[q-1] - gt[q] (q = 0: pos - gt[0]); warp sums, then one smem add per warp
+#pragma unroll
+  for (int q = 0; q < NB; ++q) {
+    int c = (q == 0 ? pos : gt[q - 1]) - gt[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c && q < p.nb) atomicAdd(&cnt[q], c);
   }
   __syncthreads();
   if (threadIdx.x < NB) p.tile_counts[(int64_t)tile * kMaxStrata + threadIdx.x] = threadIdx.x < p.nb ? cnt[threadIdx.x] : 0;
