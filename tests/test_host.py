@@ -186,3 +186,24 @@ def test_acceptance_criteria_07_08_timeline():
     # criterion 8 (test_acceptance.py:161-165): B=2, comp [2, 2], comm [3, 3]
     assert tc.schedule_total([2, 2], [3, 3], [0, 0], 0.0, 0.0, "after_allreduce") == 8.0
     assert tc.schedule_total([2, 2], [3, 3], [0, 0], 0.0, 0.0, "before_allreduce") == 10.0
+
+
+def test_fused_sync_host_chunks_cover_layout_in_backward_order():
+    """FusedBucketSync.sync_host's chunk plan (host logic): consecutive buckets in
+    reverse order, each chunk one contiguous range, together covering [0, D)."""
+    from paper_2402_02447_b200 import capped_bucket_layout
+    from paper_2402_02447_b200.ddp import FusedBucketSync
+
+    for dim, cap, cb in ((335_141_888, 6_553_600, 4), (1000, 96, 3), (1000, 96, 1), (64, 8, 128)):
+        fs = object.__new__(FusedBucketSync)  # no device state needed for the plan
+        fs.layout = capped_bucket_layout(dim, cap)
+        chunks = fs._host_chunks(cb)
+        edge = dim
+        seen = []
+        for c0, n, offs, lens, a, b in chunks:
+            assert b == edge and a < b  # walks down from the end without gaps
+            seen += list(range(len(fs.layout) - 1 - c0, len(fs.layout) - 1 - c0 - n, -1))
+            assert [int(x) for x in offs] == [fs.layout[q][0] for q in seen[-n:]]
+            assert sum(int(x) for x in lens) == b - a
+            edge = a
+        assert edge == 0 and seen == list(range(len(fs.layout) - 1, -1, -1))
