@@ -553,14 +553,15 @@ static int clip_allreduce_impl(const void* in, void* const* stages, void* mc_sta
 
   // roles: comm CTAs on the first `cs` SMs (B2_COMM_SMS overrides), clip CTAs
   // on the rest.  Sweeps (profiles/r01_k4_split_sweep.jsonl): P2P best at 64
-  // of 148 SMs for N = 2 and 4, NVLS at 32.
+  // of 148 SMs for N = 2, 48 for N = 4 (1.63 vs 1.67-1.70 ms at 64), NVLS at 32.
+  // Twice the reduce vectors in flight per thread measured slower for both.
   cudaStream_t st = (cudaStream_t)stream;
   static int csms = -1;
   if (csms < 0) {
     const char* e = getenv("B2_COMM_SMS");
     csms = e ? atoi(e) : 0;
   }
-  const int cs = csms > 0 ? csms : (mc_stage ? 32 : 64);
+  const int cs = csms > 0 ? csms : (mc_stage ? 32 : nranks <= 2 ? 64 : 48);
   // each reduce thread keeps UC x RMAX 16 B vectors in flight (32 registers)
   if (mc_stage) return launch_split<192, 320, 8, 4, 8, 1, true>(f, st, cs);
   if (nranks <= 2) return launch_split<192, 320, 8, 4, 4, 2>(f, st, cs);
