@@ -306,3 +306,28 @@ def test_sync_bucketwise_host_streamed_matches_reference():
     got2 = sync_bucketwise_host(w2, equal_bucket_layout(500, 5), ClipConfig(1.0, "bucket_wise"))
     ref2 = O.sync_bucketwise(w2, equal_bucket_layout(500, 5), 1.0)
     assert np.abs(got2 - ref2).max() <= 1e-12 * np.abs(ref2).max()
+
+
+def test_sync_bucketwise_host_bert_large():
+    """Host-resident streamed step at BERT-large size (335 M fp32 elements, 52
+    buckets): equal to the GradientState path within fp32 tolerance; every
+    clipped bucket lands on the limit."""
+    from paper_2402_02447_b200 import sync_bucketwise_host
+
+    dim = synthetic.BERT_LARGE_DIM
+    g, layout, _ = synthetic.bert_grads(dim)
+    host = g.view(1, -1).cpu().pin_memory()
+    cfg = ClipConfig(1.0, "bucket_wise")
+    got = sync_bucketwise_host(host, layout, cfg)
+    ref = sync_bucketwise(GradientState(host, layout), cfg)
+    scale = np.abs(ref).max()
+    assert np.abs(got - ref).max() <= 1e-6 * scale
+    limit = 1.0 / math.sqrt(len(layout))
+    gh = host.view(-1).numpy()
+    for a, b in layout:
+        n_in = np.linalg.norm(gh[a:b].astype(np.float64))
+        n_out = np.linalg.norm(got[a:b].astype(np.float64))
+        if n_in >= limit:
+            assert abs(n_out - limit) <= 1e-5 * limit
+        else:
+            assert np.array_equal(got[a:b], gh[a:b])  # below the limit: the input, untouched
