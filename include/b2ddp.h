@@ -119,11 +119,15 @@ int b2_bucket_clip_allreduce(b2_comm* comm, const void* in, int in_dtype, void* 
                              double* norms, int32_t* nonfinite, void* workspace, size_t workspace_bytes,
                              void* stream, void* comm_stream);
 
-/* Fused H1 step over NVLink peer memory (no NCCL): ONE persistent kernel per
- * rank computes each bucket's norm, clips + casts it to bf16 into this rank's
- * symmetric stage buffer, and runs a two-shot allreduce of the bucket (this
- * rank reduces its 1/N slice from every stage, writes the mean into every
- * stage).  stages[q] / flags[q] ([host] arrays of nranks device pointers) are
+/* Fused H1 step over NVLink peer memory (no NCCL), K4: ONE persistent
+ * cooperative kernel per rank.  CTAs on the clip SMs compute each bucket's
+ * norm and clip + cast it to bf16 into this rank's symmetric stage buffer;
+ * CTAs on the comm SMs (64 at N=2, 48 at N=4, 32 with NVLS; B2_COMM_SMS
+ * overrides) run a two-shot allreduce of each bucket as soon as every rank
+ * has staged it (this rank reduces its 1/N slice from every stage in fixed
+ * rank order and writes the mean into every stage).  Replaces, for rank r =
+ * worker row r, sync_bucketwise's per-bucket clip + allreduce_mean
+ * (gradsync.py:148-162, :119-128).  stages[q] / flags[q] ([host] arrays of nranks device pointers) are
  * rank q's bf16 stage (D elements, buckets at seg_off) and its flag area
  * (b2_p2p_flag_bytes(), zeroed once) as mapped in this process (b2_ipc_*).
  * On return of the launch (stream order) stages[rank] holds the averaged,
