@@ -7,14 +7,21 @@
 // (_from_per_gpu, :54-56).  assign_global_presort (:83-88) is the same with a
 // single pool.
 //
-// One CTA per pool (grid-stride over pools).  The composite key
-//     ((max_len - len) << id_bits) | id
-// orders exactly like (-len, id); equal keys are identical samples, so the
-// order among them cannot change the output.  The key is sorted with an
-// in-register/shared-memory LSD radix sort limited to the bits the key
-// actually spans (cub::BlockRadixSort), then each sorted slot is dealt to
-// (lane, row) and staged in shared memory so the [lanes][rows] output tile is
-// written with consecutive addresses; token sums read the staged lengths.
+// The composite key ((max_len - len) << id_bits) | id orders exactly like
+// (-len, id); equal keys are identical samples, so the order among them
+// cannot change the output.  Three paths, all equal to the reference:
+//   * counting sort, one warp per pool (lengths <= 1024, the pool fills at
+//     least half the length bins, e.g. 384-key pools): length histogram with
+//     ranks from the atomics, warp scan, scatter, ids ordered inside
+//     equal-length bins;
+//   * bitonic network, one warp per pool (pools <= 512, e.g. 128-key pools):
+//     64-bit composite keys in registers, shuffles across lanes;
+//   * stable LSD radix sort, one CTA per pool (any pool <= 4096, and the only
+//     path that also returns each sample's input slot): cub::BlockRadixSort
+//     limited to the bits the key actually spans.
+// Each sorted slot is dealt to (lane, row) and staged in shared memory so the
+// [lanes][rows] output tile is written with consecutive addresses; token sums
+// read the staged lengths.
 #include "bitonic.cuh"
 #include "common.cuh"
 
