@@ -12,7 +12,10 @@
 //   (buckets) with two streams per CTA — A: norm pass over bucket s (128-bit
 //   loads, L2 evict_last), B: scale pass over bucket s-1 (L2 re-read,
 //   evict_first) — so the grid-wide norm dependency of a bucket is hidden
-//   behind a whole bucket of A work.  Partials are published fire-and-forget
+//   behind a whole bucket of A work.  Several buckets per launch: A and B are
+//   concurrent warp groups of every CTA (k_bucket_clip_ws, 192 + 320
+//   threads; small buckets form CTA groups, each owning every R-th bucket);
+//   a lone bucket (the DDP-hook shape): the time-sliced k_bucket_clip_l2lag.  Partials are published fire-and-forget
 //   and every CTA folds them in one fixed order (bit-deterministic, identical
 //   coefficient grid-wide).  A TMA-ring variant (cp.async.bulk into a
 //   shared-memory ring, warp-specialised producer) is kept for A/B runs
