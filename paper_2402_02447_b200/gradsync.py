@@ -265,12 +265,14 @@ def clip_by_norm(g, limit: float):
     """Rescale g to L2 norm ``limit`` iff its norm reaches the limit (gradsync.py:106-116)."""
     if limit <= 0:
         raise ValueError(f"limit must be > 0, got {limit}")
+    arr = None
     if isinstance(g, torch.Tensor):
         host = not g.is_cuda
         v = g if g.dtype in (torch.float32, torch.float64) else g.to(torch.float64)
     else:
         host = True
-        v = torch.from_numpy(np.ascontiguousarray(np.asarray(g, dtype=float)))
+        arr = np.asarray(g, dtype=float)  # a float64 ndarray comes back as itself (:110)
+        v = torch.from_numpy(np.ascontiguousarray(arr))
     src = v
     v = v.reshape(-1).to("cuda").contiguous()
     c = _clipper()
@@ -281,7 +283,9 @@ def clip_by_norm(g, limit: float):
     _raise_if_flagged(flags)
     if float(norms.item()) >= limit:
         return _result(out.reshape(src.shape), host)
-    return src.numpy() if host else src  # unchanged: the input itself (:116)
+    if arr is not None:
+        return arr  # unchanged: the same array object (:116)
+    return src.numpy() if host else src
 
 
 def allreduce_mean(workers):

@@ -96,6 +96,9 @@ def test_clip_kats():
     np.testing.assert_allclose(clip_by_norm(np.array([3.0, 4.0]), 1.0), [0.6, 0.8], atol=1e-15)
     g = np.array([3.0, 4.0])
     np.testing.assert_array_equal(clip_by_norm(g, 10.0), g)
+    assert clip_by_norm(g, 10.0) is g  # not clipped: the same array object (gradsync.py:116)
+    t = torch.tensor([3.0, 4.0], device="cuda")
+    assert clip_by_norm(t, 10.0) is t
     np.testing.assert_array_equal(clip_by_norm(np.zeros(4), 0.5), np.zeros(4))
     # inclusive edge: norm == limit -> coefficient exactly 1 (test_gradsync.py:42-44)
     np.testing.assert_array_equal(clip_by_norm(np.array([0.0, 2.0]), 2.0), [0.0, 2.0])
