@@ -334,3 +334,33 @@ def test_sync_bucketwise_host_bert_large():
             assert abs(n_out - limit) <= 1e-5 * limit
         else:
             assert np.array_equal(got[a:b], gh[a:b])  # below the limit: the input, untouched
+
+
+def test_state_construction_kats():
+    """TestStateConstruction (test_gradsync.py:215-253) on the CUDA state."""
+    from paper_2402_02447_b200 import gradient_state_from_dict
+
+    with pytest.raises(ValueError, match="covering"):
+        GradientState(np.ones((2, 6)), ((0, 3), (4, 6)))
+    with pytest.raises(ValueError, match="covers"):
+        GradientState(np.ones((2, 6)), ((0, 3), (3, 5)))
+    with pytest.raises(ValueError, match="at least one bucket"):
+        GradientState(np.ones((2, 6)), ())
+    with pytest.raises(ValueError, match="non-finite"):
+        GradientState(np.array([[1.0, np.nan]]), ((0, 2),))
+    st = gradient_state_from_dict({"workers": [[1, 2, 3, 4], [5, 6, 7, 8]], "bucket_layout": [[0, 2], [2, 4]]})
+    assert st.num_workers == 2 and st.num_buckets == 2 and st.dim == 4
+    st = gradient_state_from_dict({"workers": [[1, 2, 3, 4]], "num_buckets": 2})
+    assert st.bucket_layout == ((0, 2), (2, 4))
+    # every clip mode through the dispatcher on a from_dict state (synchronize, gradsync.py:165-174)
+    w = [[3.0, 4.0, 0.0, 1.0], [0.5, 0.0, 2.0, 2.0]]
+    for mode in ("after_allreduce", "before_allreduce", "bucket_wise"):
+        got = synchronize(gradient_state_from_dict({"workers": w, "num_buckets": 2}), ClipConfig(1.0, mode))
+        W = np.array(w)
+        if mode == "after_allreduce":
+            ref = O.clip_by_norm(O.allreduce_mean(W), 1.0)
+        elif mode == "before_allreduce":
+            ref = O.allreduce_mean(np.stack([O.clip_by_norm(r, 1.0) for r in W]))
+        else:
+            ref = O.sync_bucketwise(W, ((0, 2), (2, 4)), 1.0)
+        np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-15)
