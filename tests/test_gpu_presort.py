@@ -321,3 +321,37 @@ def test_presort_paths_agree_with_heavy_ties(lenrange, seg_len, lanes):
     ro, rt = O.presort_deal_segments(ids.reshape(-1), lens.reshape(-1), seg_len, lanes, True)
     np.testing.assert_array_equal(outs[0][0], ro)
     np.testing.assert_array_equal(outs[0][1], rt)
+
+
+def test_strategy_properties_conservation_and_snake():
+    """TestStrategyProperties (test_balance.py:173-216) on the K3 path:
+    conservation + exact token counts over random corpora (hypothesis), and
+    snake never worse than raster over 1,000 random global deals."""
+    from collections import Counter
+
+    from hypothesis import given, settings
+    from hypothesis import strategies as hst
+
+    @given(lengths=hst.lists(hst.integers(1, 512), min_size=1, max_size=96), gpus=hst.sampled_from([1, 2, 4]))
+    @settings(max_examples=100, deadline=None)
+    def conservation(lengths, gpus):
+        usable = len(lengths) - len(lengths) % gpus
+        if usable == 0:
+            return
+        samples = make(lengths[:usable])
+        expected = Counter(s.id for s in samples)
+        for scan in ("raster", "snake"):
+            a = assign_global_presort(samples, Topology(1, gpus), scan)
+            assert Counter(s.id for gpu in a.per_gpu for s in gpu) == expected
+            assert a.token_counts == tuple(sum(s.length for s in gpu) for gpu in a.per_gpu)
+            assert sum(a.token_counts) == sum(s.length for s in samples)
+
+    conservation()
+    rng = np.random.default_rng(424242)
+    for _ in range(1000):
+        gpus = int(rng.choice([2, 4, 8]))
+        rows = int(rng.integers(1, 9))
+        samples = make(rng.integers(1, 513, size=gpus * rows))
+        raster = assign_global_presort(samples, Topology(1, gpus), "raster")
+        snake = assign_global_presort(samples, Topology(1, gpus), "snake")
+        assert max(snake.token_counts) - min(snake.token_counts) <= max(raster.token_counts) - min(raster.token_counts)
