@@ -207,3 +207,23 @@ def test_fused_sync_host_chunks_cover_layout_in_backward_order():
             assert sum(int(x) for x in lens) == b - a
             edge = a
         assert edge == 0 and seen == list(range(len(fs.layout) - 1, -1, -1))
+
+
+def test_allocate_counts_apportionment_stability():
+    """test_strata.py:86-97: counts sum to the batch and each is within 1 of its quota."""
+    import numpy as np
+    from hypothesis import given, settings
+    from hypothesis import strategies as hst
+
+    @given(probs=hst.lists(hst.floats(0.0, 1.0), min_size=1, max_size=8).filter(lambda p: sum(p) > 1e-6),
+           batch=hst.integers(0, 200))
+    @settings(max_examples=200, deadline=None)
+    def prop(probs, batch):
+        alloc = B.allocate_counts(probs, batch)
+        assert sum(alloc.counts) == batch
+        quotas = batch * np.asarray(probs) / sum(probs)
+        assert all(abs(c - q) < 1.0 for c, q in zip(alloc.counts, quotas))
+
+    prop()
+    with pytest.raises(ValueError):
+        B.StratumAllocation((1, 1), 3)
