@@ -564,6 +564,12 @@ static int clip_allreduce_impl(const void* in, void* const* stages, void* mc_sta
   const int cs = csms > 0 ? csms : (mc_stage ? 32 : nranks <= 2 ? 64 : 48);
   // each reduce thread keeps UC x RMAX 16 B vectors in flight (32 registers)
   if (mc_stage) return launch_split<192, 320, 8, 4, 8, 1, true>(f, st, cs);
+  static int force8 = -1;  // B2_K4_FORCE_R8=1: the 8-rank build at any N (tests that path on <= 4 GPUs)
+  if (force8 < 0) {
+    const char* e = getenv("B2_K4_FORCE_R8");
+    force8 = e ? atoi(e) : 0;
+  }
+  if (force8) return launch_split<192, 320, 8, 4, 1, 8>(f, st, cs);
   if (nranks <= 2) return launch_split<192, 320, 8, 4, 4, 2>(f, st, cs);
   if (nranks <= 4) return launch_split<192, 320, 8, 4, 2, 4>(f, st, cs);
   return launch_split<192, 320, 8, 4, 1, 8>(f, st, cs);
