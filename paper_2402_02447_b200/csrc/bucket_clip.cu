@@ -631,7 +631,7 @@ __global__ void __launch_bounds__(AT + BT, CPS) k_bucket_clip_ws(const __grid_co
       unsigned ns = 32;
       while (ld_acquire_u32(&p.counters[s]) < (unsigned)G) {
         __nanosleep(ns);
-        if (ns < 256) ns <<= 1;
+        if (ns < 32) ns <<= 1;
       }
     }
     group_sync<NTH>(bar);
@@ -661,7 +661,7 @@ __global__ void __launch_bounds__(AT + BT, CPS) k_bucket_clip_ws(const __grid_co
           unsigned ns = 32;
           while (s_bdone < i - LAG) {
             __nanosleep(ns);
-            if (ns < 256) ns <<= 1;
+            if (ns < 32) ns <<= 1;
           }
         }
         group_sync<AT>(kBarA);
