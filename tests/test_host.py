@@ -227,3 +227,34 @@ def test_allocate_counts_apportionment_stability():
     prop()
     with pytest.raises(ValueError):
         B.StratumAllocation((1, 1), 3)
+
+
+def test_c_abi_from_plain_c(tmp_path):
+    """The boundary from a non-Python caller: a C program includes
+    include/b2ddp.h, links libb2ddp.so and calls host entry points
+    (b2_version, b2_derive_seed == numpy's SeedSequence, seeding.py:18-21)."""
+    import shutil
+    import subprocess
+
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    root = Path(__file__).resolve().parent.parent
+    lib = root / "paper_2402_02447_b200" / "_native"
+    src = tmp_path / "abi.c"
+    src.write_text(r'''
+#include <stdio.h>
+#include <inttypes.h>
+#include "b2ddp.h"
+int main(void) {
+  const uint64_t key[2] = {3, 17};
+  printf("%s\n%" PRIu64 "\n", b2_version(), b2_derive_seed(2402, key, 2));
+  return 0;
+}
+''')
+    exe = tmp_path / "abi"
+    subprocess.run(["gcc", "-std=c99", "-I", str(root / "include"), str(src), "-L", str(lib), "-lb2ddp",
+                    f"-Wl,-rpath,{lib}", "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.splitlines()
+    assert out[0]  # the version string
+    ref = int(np.random.SeedSequence(entropy=2402, spawn_key=(3, 17)).generate_state(1, np.uint64)[0])
+    assert int(out[1]) == ref
