@@ -85,7 +85,7 @@ int b2_bucket_clip_cast(const void* in, int in_dtype, void* out, int out_dtype,
  * A coefficient of exactly 1 leaves the element untouched (clip_by_norm
  * returns g itself, :116).  `bounds` is a [host] array of B+1 bucket edges
  * (bounds[0] = 0, bounds[B] = D).  in_dtype B2_F32|B2_F64, out_dtype
- * B2_F32|B2_F64; K <= 64. */
+ * B2_F32|B2_F64; any K >= 1. */
 int b2_weighted_mean(const void* G, int in_dtype, int64_t K, int64_t D, int64_t ld,
                      const double* coef, const int64_t* bounds, int B, void* out,
                      int out_dtype, void* stream);
@@ -132,7 +132,8 @@ int b2_bucket_clip_allreduce(b2_comm* comm, const void* in, int in_dtype, void* 
  * (b2_p2p_flag_bytes(), zeroed once) as mapped in this process (b2_ipc_*).
  * On return of the launch (stream order) stages[rank] holds the averaged,
  * clipped gradient.  All ranks must issue the same calls in the same order;
- * cross-GPU waits trap after 30 s.  nranks <= 8, nseg <= 128, buckets
+ * a cross-GPU wait longer than b2_get_spin_timeout() seconds traps (default
+ * 600 s; B2_SPIN_TIMEOUT_S or b2_set_spin_timeout, 0 = wait forever).  nranks <= 8, nseg <= 128, buckets
  * 8-element aligned.  The workspace (b2_clip_workspace_bytes) also carries
  * the launch epoch, so the call is CUDA-graph replayable. */
 /* NVLS flavour: same contract, but the reduce of each slice is one
@@ -144,6 +145,11 @@ int b2_bucket_clip_allreduce_nvls(const void* in, void* const* stages, void* mc_
                                   int nranks, int rank, const int64_t* seg_off, const int64_t* seg_len, int nseg,
                                   double limit, double* norms, int32_t* nonfinite, void* workspace,
                                   size_t workspace_bytes, void* stream);
+/* Bound, in seconds, on every cross-GPU wait of the fused kernels (0 = wait
+ * forever).  Process-wide; read at each launch.  Default 600 s, or the
+ * B2_SPIN_TIMEOUT_S environment variable. */
+int b2_set_spin_timeout(double seconds);
+double b2_get_spin_timeout(void);
 size_t b2_p2p_flag_bytes(void);
 int b2_ipc_export(const void* dev_ptr, void* handle64, int64_t* offset);
 int b2_ipc_import(const void* handle64, int64_t offset, void** base, void** dev_ptr);
@@ -222,6 +228,24 @@ int b2_draw_epoch(b2_draw_state* st, const int64_t* counts, uint64_t base_seed, 
 int b2_presort_deal(const int32_t* ids, const int32_t* lens, int64_t nseg, int seg_len,
                     int lanes, int scan, int32_t max_len, int32_t max_id, int32_t* out_ids,
                     int32_t* out_pos, int64_t* tokens, int64_t* bad, void* stream);
+
+/* K5 — the same sort + deal for pools of ANY size: a device-wide stable LSD
+ * radix sort (onesweep: one upsweep histogram launch, then one
+ * decoupled-look-back pass per <= 9-bit digit) over all nseg pools at once.
+ * Replaces _sorted_desc + _deal + _from_per_gpu (balance.py:54-75) where a
+ * pool is larger than one CTA can sort: assign_global_presort (:83-88) over a
+ * whole batch, and the "stable per-rank radix sort on length keys" over a
+ * whole rank shard (lanes = 1: out_ids is the shard in (-len, id) order).
+ * Same arguments and outputs as b2_presort_deal; seg_len <= 4096 is passed
+ * to b2_presort_deal (workspace unused).  When every pool's ids are already
+ * non-decreasing (a shard in id order) the id digits are skipped on the
+ * device.  `workspace` (device, b2_presort_workspace_bytes(...) bytes; no
+ * initialisation needed) holds the key ping-pong buffers, histograms and
+ * look-back words.  seg_len < 2^30. */
+size_t b2_presort_workspace_bytes(int64_t nseg, int seg_len, int32_t max_len, int32_t max_id, int with_pos);
+int b2_presort_sort_deal(const int32_t* ids, const int32_t* lens, int64_t nseg, int seg_len, int lanes, int scan,
+                         int32_t max_len, int32_t max_id, int32_t* out_ids, int32_t* out_pos, int64_t* tokens,
+                         int64_t* bad, void* workspace, size_t workspace_bytes, void* stream);
 
 /* Monte-Carlo balance engine, host draws.
  *

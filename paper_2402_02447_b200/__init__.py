@@ -6,7 +6,15 @@ stream, DDP comm hook).  H2 (stratified local presort): ``strata`` +
 DESIGN.md.  Names mirror ``ddpsim/__init__.py:14-103`` for the in-scope paths.
 """
 
-from .balance import Assignment, ScanPattern, assign_global_presort, assign_local_presort, presort_deal
+from .balance import (
+    Assignment,
+    ScanPattern,
+    assign_global_presort,
+    assign_local_presort,
+    presort_deal,
+    presort_workspace_bytes,
+    sort_shard,
+)
 from .gradsync import (
     BucketClipper,
     ClipConfig,
@@ -52,6 +60,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "Assignment", "ScanPattern", "assign_global_presort", "assign_local_presort", "presort_deal",
+    "presort_workspace_bytes", "sort_shard",
     "BucketClipper", "ClipConfig", "ClipMode", "GradientState", "allreduce_mean",
     "capped_bucket_layout", "clip_by_norm", "equal_bucket_layout", "gradient_state_from_dict",
     "sync_after", "sync_before", "sync_bucketwise", "sync_bucketwise_host", "synchronize",

@@ -65,6 +65,13 @@ SIGNATURES = {
         _I,
         [_P, _P, _I64, _I, _I, _I, C.c_int32, C.c_int32, _P, _P, _P, _P, _P],
     ),
+    "b2_presort_workspace_bytes": (_SZ, [_I64, _I, C.c_int32, C.c_int32, _I]),
+    "b2_presort_sort_deal": (
+        _I,
+        [_P, _P, _I64, _I, _I, _I, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _SZ, _P],
+    ),
+    "b2_set_spin_timeout": (_I, [_D]),
+    "b2_get_spin_timeout": (_D, []),
     "b2_mc_draw": (_I, [_P, _P, _I, _P, _I, C.c_uint64, _I64, _I64, _I, _P]),
     "b2_mc_token_counts": (_I, [_P, _I64, _I, _I, _I, _I, _I, C.c_int32, _P, _P, _P, _P, _P]),
     "b2_mc_draw_device": (_I, [_P, _P, _I, _P, _I, C.c_uint64, _I64, _I64, _P, _P]),

@@ -18,9 +18,8 @@
 //   a lone bucket (the DDP-hook shape): the time-sliced k_bucket_clip_l2lag.  Partials are published fire-and-forget
 //   and every CTA folds them in one fixed order (bit-deterministic, identical
 //   coefficient grid-wide).  A TMA-ring variant (cp.async.bulk into a
-//   shared-memory ring, warp-specialised producer) is kept for A/B runs
-//   (B2_CLIP_CFG=5); measured slower on B200 because the ring must either hold
-//   the bucket through the barrier or lose its L2 residency.
+//   shared-memory ring) measured slower on B200 because the ring must either
+//   hold the bucket through the barrier or lose its L2 residency.
 #include "clip_common.cuh"
 
 #include <cuda_bf16.h>
@@ -32,343 +31,6 @@
 namespace b2 {
 namespace {
 using namespace clip;
-
-// ----------------------------------------------------------------------------
-// K1 (TMA ring): 1 CTA per SM; each CTA's chunk of a bucket is pulled into a
-// shared-memory ring of 16 KB pieces by cp.async.bulk (TMA), each piece with
-// its own mbarrier.  The chunk stays on chip until the bucket's coefficient is
-// published, is then scaled straight out of shared memory, and every freed
-// piece is immediately refilled with the next bucket's data — so the DMA
-// engine keeps HBM busy through the norm barrier.  DRAM traffic is exactly the
-// algorithmic 4 B read + 2/4 B write per element (no L2 re-read) as long as a
-// CTA's chunk fits the ring (bucket <= #SM x 224 KB = 33 MB); larger chunks
-// spill their tail to an L2-resident re-read (evict_last / evict_first hints).
-constexpr int kTThreads = 512;
-
-__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
-  return (uint32_t)__cvta_generic_to_shared(ptr);
-}
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  uint32_t done = 0;
-  while (!done)
-    asm volatile(
-        "{ .reg .pred P; mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2; selp.u32 %0, 1, 0, P; }"
-        : "=r"(done)
-        : "r"(bar), "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void tma_load_1d(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-      "l"(src), "r"(bytes), "r"(bar)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-// consumer-only barrier (the producer warp never joins it)
-__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kTThreads) : "memory"); }
-__device__ __forceinline__ int consumer_sync_or(int pred) {
-  int r;
-  asm volatile(
-      "{ .reg .pred a, b; setp.ne.s32 a, %1, 0; bar.red.or.pred b, 1, %2, a; selp.s32 %0, 1, 0, b; }"
-      : "=r"(r)
-      : "r"(pred), "n"(kTThreads)
-      : "memory");
-  return r;
-}
-
-template <int THREADS>
-__device__ __forceinline__ double consumer_block_sum(double v, double* scratch) {
-  constexpr int W = THREADS / 32;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  v = warp_sum(v);
-  consumer_sync();
-  if (lane == 0) scratch[warp] = v;
-  consumer_sync();
-  double r = 0.0;
-  if (warp == 0) {
-    r = lane < W ? scratch[lane] : 0.0;
-    r = warp_sum(r);
-  }
-  return r;  // valid in warp 0
-}
-
-__device__ __forceinline__ void tma_load_1d_hint(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar,
-                                                 uint64_t pol) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-          dst),
-      "l"(src), "r"(bytes), "r"(bar), "l"(pol)
-      : "memory");
-}
-
-// Warp-specialised, two-stream persistent kernel (one CTA per SM).
-//   stream A (norm): warp 16 pulls this CTA's chunk of every bucket through a
-//     shared-memory ring with cp.async.bulk (TMA, L2 evict_last), warps 0..15
-//     sum squares and release each 16 KB piece at once; one fp64 partial per
-//     (bucket, CTA) is published fire-and-forget (red.release).
-//   stream B (scale): LAG buckets behind, each CTA folds bucket s's partials
-//     (fixed order -> bit-identical coefficient in every CTA), re-reads its
-//     chunk from L2 (evict_first: last use) and writes g*coef*post_scale.
-// By the time B(s) needs bucket s's coefficient the whole grid has long
-// finished A(s), so no CTA idles at the norm barrier and HBM sees exactly the
-// algorithmic traffic: the A read + the B write (B's re-read hits L2; the
-// bucket is 26 MB, L2 is 126 MB).  A lone bucket (the DDP-hook case) runs A
-// then B with one grid-wide wait in between.
-// MODE 0: stream A through the TMA ring with an L2 evict_last hint
-// MODE 1: TMA ring, default L2 policy
-// MODE 2: stream A with plain 128-bit loads (evict_last), ring unused
-template <typename Tin, typename Tout, int NP, int PIECE, int LAG, int MODE>
-__global__ void __launch_bounds__(kTThreads + 32, 1) k_bucket_clip_tma(const __grid_constant__ ClipParams p) {
-  using V = typename VecOf<Tin>::V;
-  constexpr int N = VecOf<Tin>::N;
-  constexpr bool kF64 = std::is_same<Tin, double>::value;
-  constexpr int kWarps = kTThreads / 32;
-  constexpr int PV = PIECE / 16;       // 16 B vectors per piece
-  constexpr int VPT = PV / kTThreads;  // vectors per consumer thread per piece
-  constexpr int UB = 8;                // stream-B loads in flight per thread
-  static_assert(PV % kTThreads == 0, "piece must split evenly over consumer threads");
-  using Acc = typename std::conditional<std::is_same<Tin, double>::value || std::is_same<Tout, double>::value,
-                                        double, float>::type;
-  extern __shared__ __align__(128) unsigned char ring[];
-  __shared__ double s_coef[2];
-  __shared__ double red[32];
-  const int G = gridDim.x, c = blockIdx.x, t = threadIdx.x;
-  const uint32_t ring_base = smem_u32(ring);
-  const uint32_t full_base = ring_base + NP * PIECE;
-  const uint32_t empty_base = full_base + 8u * NP;
-  const bool scale = p.out != nullptr;
-
-  if (MODE != 2 && t == 0) {  // MODE 2 launches without the ring (no dynamic smem)
-    for (int i = 0; i < NP; ++i) {
-      mbar_init(full_base + 8u * i, 1);
-      mbar_init(empty_base + 8u * i, kWarps);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-
-  if (t >= kTThreads) {
-    // ---------------- producer warp (stream A)
-    if (MODE != 2 && t == kTThreads) {
-      const uint64_t pol = scale ? l2_policy_evict_last() : l2_policy_evict_first();
-      uint32_t q = 0;
-      for (int s = 0; s < p.nseg; ++s) {
-        const Seg& sg = p.seg[s];
-        if (!sg.vec) continue;
-        const int64_t v0 = min64((int64_t)c * sg.per, sg.nv), v1 = min64(v0 + sg.per, sg.nv);
-        const char* src = reinterpret_cast<const char*>(static_cast<const Tin*>(p.in) + sg.in_off + sg.head) + v0 * 16;
-        for (int64_t off = 0; off < v1 - v0; off += PV, ++q) {
-          const uint32_t slot = q % NP, fill = q / NP;
-          if (fill > 0) mbar_wait(empty_base + 8u * slot, (fill - 1) & 1);
-          const int nvec = (int)min64(PV, v1 - v0 - off);
-          if (MODE == 0) tma_load_1d_hint(ring_base + slot * PIECE, src + off * 16, nvec * 16, full_base + 8u * slot, pol);
-          else tma_load_1d(ring_base + slot * PIECE, src + off * 16, nvec * 16, full_base + 8u * slot);
-        }
-      }
-    }
-    return;
-  }
-
-  // ---------------- consumer warps
-  const int lane = t & 31, warp = t >> 5;
-  const uint64_t pol_keep = l2_policy_evict_last();
-  const uint64_t pol_drop = l2_policy_evict_first();
-
-  // fold the G partials of segment s (warp 0, fixed order) -> coefficient
-  auto fold = [&](int s, bool publish) -> double {
-    if (lane == 0) {
-      unsigned ns = 32;
-      while (ld_acquire_u32(&p.counters[s]) < (unsigned)G) {
-        __nanosleep(ns);
-        if (ns < 256) ns <<= 1;
-      }
-    }
-    __syncwarp();
-    double v = 0.0;
-    for (int j = lane; j < G; j += 32) v += __ldcg(&p.partials[(size_t)s * G + j]);
-    const double total = warp_sum(v);
-    const double norm = sqrt(total);
-    const double coef = (norm >= p.limit) ? p.limit / norm : 1.0;  // gradsync.py:114-116
-    if (publish && lane == 0) {
-      if (p.norms) p.norms[s] = norm;
-      if (p.coefs) p.coefs[s] = coef;
-      if (p.nonfinite) p.nonfinite[s] = (kF64 ? isnan(total) : !isfinite(total)) ? 1 : 0;
-    }
-    return coef;
-  };
-
-  // ---- stream A for segment s: sum of squares, publish the CTA partial
-  uint32_t q = 0;
-  auto norm_pass = [&](int s) {
-    const Seg sg = p.seg[s];  // by value: keep the descriptor in registers
-    const Tin* in = static_cast<const Tin*>(p.in) + sg.in_off;
-    double acc[N];
-#pragma unroll
-    for (int u = 0; u < N; ++u) acc[u] = 0.0;
-    bool bad = false;
-    auto add = [&](const V& x) {  // exact fp64 accumulation
-      double e[N];
-      unpack(x, e);
-#pragma unroll
-      for (int u = 0; u < N; ++u) {
-        if constexpr (kF64) bad |= !isfinite(e[u]);
-        acc[u] = fma(e[u], e[u], acc[u]);
-      }
-    };
-    auto mini = [&](const V* xs, int cnt) {
-      if constexpr (kF64) {
-        for (int u = 0; u < cnt; ++u) add(xs[u]);
-      } else {
-        // f32: a handful of squares summed in fp32 (rel. error < 2e-6),
-        // promoted once; a mini-sum outside [2^-100, 2^100] (underflow,
-        // overflow, inf, nan) is redone exactly in fp64
-        float m = 0.0f;
-        unsigned nz = 0;
-        for (int u = 0; u < cnt; ++u) {
-          m = fmaf(xs[u].x, xs[u].x, m);
-          m = fmaf(xs[u].y, xs[u].y, m);
-          m = fmaf(xs[u].z, xs[u].z, m);
-          m = fmaf(xs[u].w, xs[u].w, m);
-          nz |= __float_as_uint(xs[u].x) | __float_as_uint(xs[u].y) | __float_as_uint(xs[u].z) |
-                __float_as_uint(xs[u].w);
-        }
-        if (m >= 0x1p-100f && m <= 0x1p100f) {
-          acc[0] += (double)m;
-        } else if ((nz << 1) != 0u) {  // some element is non-zero: exact path
-          for (int u = 0; u < cnt; ++u) add(xs[u]);
-        }
-      }
-    };
-    if (sg.vec && MODE == 2) {
-      constexpr int UA = 16;  // 128-bit loads in flight per thread
-      const V* vin = reinterpret_cast<const V*>(in + sg.head);
-      const int64_t v0 = min64((int64_t)c * sg.per, sg.nv), v1 = min64(v0 + sg.per, sg.nv);
-      for (int64_t v = v0 + t; v < v1; v += (int64_t)kTThreads * UA) {
-        V x[UA];
-#pragma unroll
-        for (int u = 0; u < UA; ++u) {
-          const int64_t vi = v + (int64_t)u * kTThreads;
-          x[u] = vi < v1 ? ld_hint(vin + vi, pol_keep) : V{};
-        }
-#pragma unroll
-        for (int h = 0; h < UA; h += 8) mini(x + h, 8);
-      }
-    }
-    if (sg.vec && MODE != 2) {
-      const int64_t v0 = min64((int64_t)c * sg.per, sg.nv), v1 = min64(v0 + sg.per, sg.nv);
-      for (int64_t off = 0; off < v1 - v0; off += PV, ++q) {
-        const uint32_t slot = q % NP;
-        mbar_wait(full_base + 8u * slot, (q / NP) & 1);
-        const int nvec = (int)min64(PV, v1 - v0 - off);
-        const V* sp = reinterpret_cast<const V*>(ring + slot * PIECE);
-        V xs[VPT];
-#pragma unroll
-        for (int u = 0; u < VPT; ++u) {
-          const int i = t + u * kTThreads;
-          xs[u] = i < nvec ? sp[i] : V{};
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty_base + 8u * slot);  // piece consumed: refill at once
-        mini(xs, VPT);
-      }
-    }
-    if (sg.vec) {
-      const int64_t tail0 = sg.head + sg.nv * N;
-      if (c == 0 && t < sg.head) acc[0] += sq_of(in[t], bad);
-      if (c == G - 1 && t < sg.n - tail0) acc[N - 1] += sq_of(in[tail0 + t], bad);
-    } else {
-      const int64_t per = (sg.n + G - 1) / G;
-      const int64_t e0 = min64((int64_t)c * per, sg.n), e1 = min64(e0 + per, sg.n);
-      for (int64_t e = e0 + t; e < e1; e += kTThreads) acc[0] += sq_of(in[e], bad);
-    }
-    double part = 0.0;
-#pragma unroll
-    for (int u = 0; u < N; ++u) part += acc[u];
-    double tot = consumer_block_sum<kTThreads>(part, red);
-    if constexpr (kF64) {
-      if (consumer_sync_or(bad)) tot = __longlong_as_double(0x7ff8000000000000ll);  // NaN marks inf/nan input
-    }
-    if (t == 0) {
-      p.partials[(size_t)s * G + c] = tot;
-      red_release_u32(&p.counters[s], 1u);  // fire-and-forget arrival
-    }
-  };
-
-  // ---- stream B for segment s: coefficient, L2 re-read, scale + cast + store
-  auto scale_pass = [&](int s) {
-    const Seg sg = p.seg[s];
-    if (warp == 0) {
-      const double coef = fold(s, c == 0);
-      if (lane == 0) s_coef[s & 1] = coef;
-    }
-    consumer_sync();
-    const Acc cf = static_cast<Acc>(s_coef[s & 1] * p.post_scale);
-    const Tin* in = static_cast<const Tin*>(p.in) + sg.in_off;
-    Tout* out = static_cast<Tout*>(p.out) + sg.out_off;
-    auto put = [&](int64_t v, const V& x) {
-      Acc y[N];
-      if constexpr (kF64) {
-        y[0] = x.x * cf;
-        y[1] = x.y * cf;
-      } else {  // f32 in: scale in the output's working precision
-        y[0] = static_cast<Acc>(x.x) * cf;
-        y[1] = static_cast<Acc>(x.y) * cf;
-        y[2] = static_cast<Acc>(x.z) * cf;
-        y[3] = static_cast<Acc>(x.w) * cf;
-      }
-      put_vec<Tout, N, Acc>(out + sg.head + v * N, y);
-    };
-    if (sg.vec) {
-      const V* vin = reinterpret_cast<const V*>(in + sg.head);
-      const int64_t v0 = min64((int64_t)c * sg.per, sg.nv), v1 = min64(v0 + sg.per, sg.nv);
-      for (int64_t v = v0 + t; v < v1; v += (int64_t)kTThreads * UB) {
-        V x[UB];
-#pragma unroll
-        for (int u = 0; u < UB; ++u) {
-          const int64_t vi = v + (int64_t)u * kTThreads;
-          if (vi < v1) x[u] = ld_hint(vin + vi, pol_drop);
-        }
-#pragma unroll
-        for (int u = 0; u < UB; ++u) {
-          const int64_t vi = v + (int64_t)u * kTThreads;
-          if (vi < v1) put(vi, x[u]);
-        }
-      }
-      const int64_t tail0 = sg.head + sg.nv * N;
-      if (c == 0 && t < sg.head) put1(out + t, static_cast<Acc>(in[t]) * cf);
-      if (c == G - 1 && t < sg.n - tail0) put1(out + tail0 + t, static_cast<Acc>(in[tail0 + t]) * cf);
-    } else {
-      const int64_t per = (sg.n + G - 1) / G;
-      const int64_t e0 = min64((int64_t)c * per, sg.n), e1 = min64(e0 + per, sg.n);
-      for (int64_t e = e0 + t; e < e1; e += kTThreads) put1(out + e, static_cast<Acc>(in[e]) * cf);
-    }
-  };
-
-  for (int it = 0; it < p.nseg + (scale ? LAG : 0); ++it) {
-    if (it < p.nseg) norm_pass(it);
-    if (scale && it >= LAG) scale_pass(it - LAG);
-  }
-
-  // norm-only launches: publish every segment's norm / coefficient, spread over CTAs
-  if (!scale && warp == 0)
-    for (int s = c; s < p.nseg; s += G) fold(s, true);
-
-  consumer_sync();
-  if (t == 0) {
-    if (atom_add_acq_rel_u32(&p.counters[kMaxSegs], 1u) == (unsigned)G - 1) {
-      for (int s = 0; s < p.nseg; ++s) p.counters[s] = 0u;
-      p.counters[kMaxSegs] = 0u;
-      __threadfence();
-    }
-  }
-}
 
 // ----------------------------------------------------------------------------
 // K1 (L2-lag): the production variant.  Persistent cooperative grid of CPS
@@ -842,98 +504,22 @@ int launch_ws(ClipParams& p, cudaStream_t stream) {
   return B2_OK;
 }
 
-constexpr int kRingPieces = 13;  // 13 x 16 KB = 208 KB ring (+ barriers) per SM
-constexpr int kPiece = 16384;
-
-template <typename Tin, typename Tout, int LAG, int MODE>
-int launch_clip_tma_lag(ClipParams& p, cudaStream_t stream) {
-  auto kern = k_bucket_clip_tma<Tin, Tout, kRingPieces, kPiece, LAG, MODE>;
-  const DeviceInfo& di = device_info();
-  B2_REQUIRE(di.coop, B2_ERR_CUDA, "device does not support cooperative launch");
-  constexpr int smem = MODE == 2 ? 0 : kRingPieces * (kPiece + 16);
-  static bool configured[64] = {};
-  if (!configured[di.device & 63]) {  // one-time per device and instantiation
-    B2_CHECK(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    int occ = 0;
-    B2_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kTThreads + 32, smem));
-    B2_REQUIRE(occ >= 1, B2_ERR_CUDA, "TMA clip kernel cannot be resident");
-    configured[di.device & 63] = true;
-  }
-  int64_t total = 0;
-  for (int s = 0; s < p.nseg; ++s) total += p.seg[s].n;
-  // small problems use fewer CTAs (>= four 16 KB pieces of elements each)
-  const int64_t want = (total + 16384 - 1) / 16384;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)di.sm_count, want, (int64_t)kMaxGrid}));
-  const int N = p.seg_vec_elems;
-  for (int s = 0; s < p.nseg; ++s) {  // per-CTA chunk geometry (host-side division)
-    Seg& sg = p.seg[s];
-    sg.nv = sg.vec ? (sg.n - sg.head) / N : 0;
-    sg.per = (sg.nv + grid - 1) / grid;
-  }
-  // cooperative (all CTAs co-resident: they wait on each other's partials);
-  // cudaLaunchKernelEx keeps the launch capturable into CUDA graphs
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kTThreads + 32);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  B2_CHECK(cudaLaunchKernelEx(&cfg, kern, p));
-  return B2_OK;
-}
-
-static int clip_cfg() {
-  // tuning knob: B2_CLIP_CFG selects a K1 configuration (see launch_clip_tma)
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("B2_CLIP_CFG");
-    v = e ? atoi(e) : 0;
-  }
-  return v;
-}
-
 // K1 configuration (tools/clip_bench.py sweeps; measurements in DESIGN.md):
 // several buckets per launch -> warp-specialised two-stream kernel
 // (192 norm + 320 scale threads, 2 CTAs/SM: the latency-bound L2 re-read
 // stream gets the larger group); a lone bucket (DDP-hook shape)
 // -> the time-sliced L2-lag kernel, which has the shorter critical path.
-// B2_CLIP_CFG overrides for A/B runs (5 = TMA ring, 10 = L2-lag, 20.. = ws).
+// (The measured alternatives — a TMA shared-memory ring and other warp
+// splits — live in git history, commit 4cd4b3b, not in the product library.)
 template <typename Tin, typename Tout>
 int launch_clip_k1(ClipParams& p, cudaStream_t stream) {
-  if constexpr (std::is_same<Tin, float>::value && std::is_same<Tout, __nv_bfloat16>::value) {
-    switch (clip_cfg()) {
-      case 5: return launch_clip_tma_lag<Tin, Tout, 1, 0>(p, stream);
-      case 10: return launch_l2lag<Tin, Tout, 384, 2, 1, 8, 4, 0>(p, stream);
-      case 20: return launch_ws<Tin, Tout, 256, 256, 2, 1, 8, 4>(p, stream);
-      case 21: return launch_ws<Tin, Tout, 320, 192, 2, 1, 8, 4>(p, stream);
-      case 22: return launch_ws<Tin, Tout, 384, 128, 2, 1, 8, 4>(p, stream);
-      case 23: return launch_ws<Tin, Tout, 192, 320, 2, 1, 8, 4>(p, stream);
-      case 24: return launch_ws<Tin, Tout, 128, 128, 4, 1, 8, 4>(p, stream);
-      case 25: return launch_ws<Tin, Tout, 256, 256, 2, 2, 8, 4>(p, stream);
-      case 26: return launch_ws<Tin, Tout, 256, 256, 2, 1, 4, 4>(p, stream);
-      case 27: return launch_ws<Tin, Tout, 160, 352, 2, 1, 8, 4>(p, stream);
-      case 28: return launch_ws<Tin, Tout, 128, 384, 2, 1, 8, 4>(p, stream);
-      case 29: return launch_ws<Tin, Tout, 224, 288, 2, 1, 8, 4>(p, stream);
-      case 30: return launch_ws<Tin, Tout, 192, 320, 2, 1, 8, 2>(p, stream);
-      case 31: return launch_ws<Tin, Tout, 192, 320, 2, 1, 12, 4>(p, stream);
-      case 32: return launch_ws<Tin, Tout, 192, 320, 2, 0, 8, 4>(p, stream);
-      case 33: return launch_ws<Tin, Tout, 192, 320, 2, 2, 8, 4>(p, stream);
-      case 34: return launch_ws<Tin, Tout, 384, 640, 1, 1, 8, 4>(p, stream);
-      case 35: return launch_ws<Tin, Tout, 192, 320, 2, 1, 8, 8>(p, stream);
-      default: break;
-    }
-  }
   // norm-only launches have no scale stream: the time-sliced kernel puts every thread on the norm
   if (p.nseg >= 2 && p.out != nullptr) return launch_ws<Tin, Tout, 192, 320, 2, 1, 8, 4>(p, stream);
   return launch_l2lag<Tin, Tout, 384, 2, 1, 8, 4, 0>(p, stream);
 }
 
 // ---------------------------------------------------------------- K1b
-constexpr int kMaxK = 64;
+constexpr int kCoefSmem = 256;  // coefficients staged in shared memory (more: read through L1)
 constexpr int kMeanThreads = 256;
 
 struct MeanParams {
@@ -945,28 +531,42 @@ struct MeanParams {
   int64_t bounds[kMaxSegs + 1];
 };
 
+// The reference's pairwise tree (gradsync.py:123-127: each round merges
+// (0,1),(2,3).., an odd tail is carried) equals a binary-counter stack walk in
+// ascending worker order: push each value as a block of size 1, merge the top
+// two while they have equal sizes, and at the end fold the stack from the top
+// (right to left).  Every addition has the same operands in the same order,
+// so the result is bit-identical for any K, with a stack of log2(K)+1 slots
+// instead of K registers.
 template <typename Tin, typename Tout>
 __global__ void __launch_bounds__(kMeanThreads) k_weighted_mean(const __grid_constant__ MeanParams p) {
-  __shared__ double cf[kMaxK];
+  __shared__ double cf[kCoefSmem];
   const int b = p.b0 + blockIdx.y;
-  const int K = (int)p.K;
-  if (threadIdx.x < K) cf[threadIdx.x] = p.coef[(int64_t)threadIdx.x * p.B_total + b];
+  const int64_t K = p.K;
+  for (int k = threadIdx.x; k < K && k < kCoefSmem; k += kMeanThreads) cf[k] = p.coef[(int64_t)k * p.B_total + b];
   __syncthreads();
   const int64_t lo = p.bounds[blockIdx.y], hi = p.bounds[blockIdx.y + 1];
   const Tin* g = static_cast<const Tin*>(p.G);
   Tout* out = static_cast<Tout*>(p.out);
   for (int64_t i = lo + (int64_t)blockIdx.x * kMeanThreads + threadIdx.x; i < hi;
        i += (int64_t)gridDim.x * kMeanThreads) {
-    double v[kMaxK];
-    for (int k = 0; k < K; ++k) v[k] = static_cast<double>(g[(int64_t)k * p.ld + i]) * cf[k];
-    int n = K;  // pairwise tree over ascending worker index (gradsync.py:123-127)
-    while (n > 1) {
-      int m = 0;
-      for (int j = 0; j + 1 < n; j += 2) v[m++] = v[j] + v[j + 1];
-      if (n & 1) v[m++] = v[n - 1];
-      n = m;
+    double st[64];
+    int64_t sz[64];
+    int top = 0;
+    for (int64_t k = 0; k < K; ++k) {
+      const double c = k < kCoefSmem ? cf[k] : __ldg(&p.coef[k * p.B_total + b]);
+      double v = static_cast<double>(g[k * p.ld + i]) * c;
+      int64_t n = 1;
+      while (top > 0 && sz[top - 1] == n) {  // equal blocks: one tree merge
+        v = st[--top] + v;
+        n <<= 1;
+      }
+      st[top] = v;
+      sz[top++] = n;
     }
-    out[i] = static_cast<Tout>(v[0] / (double)K);  // mean, not sum (:128)
+    double v = st[--top];
+    while (top > 0) v = st[--top] + v;  // odd tails, folded right to left
+    out[i] = static_cast<Tout>(v / (double)K);  // mean, not sum (:128)
   }
 }
 
@@ -1023,8 +623,7 @@ extern "C" int b2_weighted_mean(const void* G, int in_dtype, int64_t K, int64_t 
                                 const double* coef, const int64_t* bounds, int B, void* out,
                                 int out_dtype, void* stream) {
   B2_REQUIRE(G && coef && bounds && out, B2_ERR_INVALID, "NULL pointer argument");
-  B2_REQUIRE(K >= 1 && K <= kMaxK, B2_ERR_UNSUPPORTED, "K must be in [1, %d], got %lld", kMaxK,
-             (long long)K);
+  B2_REQUIRE(K >= 1, B2_ERR_INVALID, "K must be >= 1, got %lld", (long long)K);
   B2_REQUIRE(B >= 1 && D >= 1 && ld >= D, B2_ERR_INVALID, "bad shape");
   B2_REQUIRE(bounds[0] == 0 && bounds[B] == D, B2_ERR_INVALID, "bounds must cover [0, D)");
   B2_REQUIRE(in_dtype == B2_F32 || in_dtype == B2_F64, B2_ERR_INVALID, "bad in_dtype");

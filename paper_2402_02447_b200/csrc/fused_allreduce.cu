@@ -28,7 +28,7 @@
 // off the clip SMs.  The launch ends when this rank has seen every rank's done
 // flag, so the local stage then holds the averaged clipped gradient.  Flags
 // carry a per-launch epoch (no resets); every cross-GPU wait is bounded (trap
-// after 30 s instead of a hang).
+// after B2_SPIN_TIMEOUT_S, default 10 min, 0 = unbounded).
 #include "clip_common.cuh"
 
 #include <cuda_bf16.h>
@@ -42,7 +42,13 @@ using namespace clip;
 
 constexpr int kMaxRanks = 8;
 constexpr int kBarA = 1, kBarB = 2;
-constexpr uint64_t kSpinTimeoutNs = 30ull * 1000 * 1000 * 1000;
+// Bound on every cross-GPU wait.  Ranks legitimately drift apart (a
+// checkpoint or eval on one rank, a slow loader), so the default is generous
+// (10 min) and 0 disables it (wait forever, like NCCL).  B2_SPIN_TIMEOUT_S or
+// b2_set_spin_timeout() set it per process; a wait that exceeds it traps
+// (sticky CUDA error) instead of hanging the job silently.
+constexpr double kDefaultSpinTimeoutS = 600.0;
+static double g_spin_timeout_s = -1.0;  // < 0: not yet read from the environment
 
 struct FusedParams {
   ClipParams p;                        // in/out/limit/segments; p.out = local stage
@@ -54,6 +60,7 @@ struct FusedParams {
   int nranks, rank;
   float inv_n;
   int comm_sms;  // split kernel: CTAs on SMs [0, comm_sms) reduce, all others clip
+  uint64_t timeout_ns;  // cross-GPU wait bound (0 = unbounded)
 };
 
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
@@ -73,13 +80,13 @@ __device__ __forceinline__ uint64_t global_ns() {
   return t;
 }
 // wait until *p has reached `epoch` (wrap-safe), bounded
-__device__ __forceinline__ void wait_epoch(const uint32_t* p, uint32_t epoch) {
+__device__ __forceinline__ void wait_epoch(const uint32_t* p, uint32_t epoch, uint64_t timeout_ns) {
   const uint64_t t0 = global_ns();
   unsigned ns = 32;
   while ((int32_t)(ld_acquire_sys(p) - epoch) < 0) {
     __nanosleep(ns);
     if (ns < 1024) ns <<= 1;
-    if (global_ns() - t0 > kSpinTimeoutNs) __trap();  // a peer never arrived: fail, do not hang
+    if (timeout_ns && global_ns() - t0 > timeout_ns) __trap();  // a peer never arrived: fail, do not hang
   }
 }
 // timeline stamps (ns) in the unused partial rows kMaxSegs-1-k of the
@@ -154,7 +161,7 @@ __global__ void __launch_bounds__(kAT + kBT, 2) k_clip_allreduce_split(const __g
     red_release_u32(&reg[2], 1u);
     const uint64_t t0 = global_ns();
     while (ld_acquire_u32(&reg[2]) < gridDim.x)
-      if (global_ns() - t0 > kSpinTimeoutNs) __trap();
+      if (f.timeout_ns && global_ns() - t0 > f.timeout_ns) __trap();
     s_nk = (int)ld_acquire_u32(&reg[0]);
     s_nc = (int)ld_acquire_u32(&reg[1]);
     if (s_nk == 0 || s_nc == 0) __trap();  // host sizes comm_sms inside the SM count
@@ -241,7 +248,12 @@ __global__ void __launch_bounds__(kAT + kBT, 2) k_clip_allreduce_split(const __g
         const double total = group_sum<kBT>(v, redB, gt, kBarB);
         if (gt == 0) {
           const double norm = sqrt(total);
-          const double coef = (norm >= p.limit) ? p.limit / norm : 1.0;  // gradsync.py:114-116
+          // gradsync.py:114-116.  A non-finite bucket (the reference raises,
+          // :111-112) is staged as all-NaN, so after the mean EVERY rank's
+          // copy of the whole bucket is NaN: any rank detects it locally
+          // (FusedBucketSync.nonfinite_buckets) without another collective.
+          const double coef = !isfinite(total) ? __longlong_as_double(0x7ff8000000000000ll)
+                              : (norm >= p.limit) ? p.limit / norm : 1.0;
           if (c == 0) {
             if (p.norms) p.norms[s] = norm;
             if (p.nonfinite) p.nonfinite[s] = !isfinite(total) ? 1 : 0;
@@ -321,7 +333,7 @@ __global__ void __launch_bounds__(kAT + kBT, 2) k_clip_allreduce_split(const __g
       // release/acquire -> the peer's loads of this rank's stage.
       if (t == kTC && NR > 1) {
         for (int s = cidx; s < p.nseg; s += NC) {
-          wait_epoch(flag(f, f.rank, 0, f.rank, s), epoch);
+          wait_epoch(flag(f, f.rank, 0, f.rank, s), epoch, f.timeout_ns);
           __threadfence_system();
           for (int q = 0; q < NR; ++q)
             if (q != f.rank) st_release_sys(flag(f, q, 0, f.rank, s), epoch);
@@ -339,7 +351,7 @@ __global__ void __launch_bounds__(kAT + kBT, 2) k_clip_allreduce_split(const __g
         if (fi < M) {
           while (fi >= s_beg[cur + 1]) ++cur;
           if (ld_acquire_cta_shared(&s_rdy[cur]) == 0u) {
-            for (int q = 0; q < NR; ++q) wait_epoch(flag(f, f.rank, 0, q, cur), epoch);
+            for (int q = 0; q < NR; ++q) wait_epoch(flag(f, f.rank, 0, q, cur), epoch, f.timeout_ns);
             st_release_cta_shared(&s_rdy[cur], 1u);
             if (cur == 0 && t == 0) stamp(p, 2);
           }
@@ -395,7 +407,7 @@ __global__ void __launch_bounds__(kAT + kBT, 2) k_clip_allreduce_split(const __g
         for (int q = 0; q < NR; ++q) st_release_sys(flag(f, q, 1, f.rank, 0), epoch);
       }
       if (cidx == 0)
-        for (int q = 0; q < NR; ++q) wait_epoch(flag(f, f.rank, 1, q, 0), epoch);
+        for (int q = 0; q < NR; ++q) wait_epoch(flag(f, f.rank, 1, q, 0), epoch, f.timeout_ns);
     }
   }
 
@@ -456,6 +468,23 @@ typedef int (*PMemGetAddressRange)(unsigned long long*, size_t*, unsigned long l
 
 using namespace b2;
 using namespace b2::clip;
+
+static double spin_timeout_s() {
+  if (g_spin_timeout_s < 0.0) {
+    const char* e = getenv("B2_SPIN_TIMEOUT_S");
+    g_spin_timeout_s = e ? atof(e) : kDefaultSpinTimeoutS;
+    if (g_spin_timeout_s < 0.0) g_spin_timeout_s = 0.0;
+  }
+  return g_spin_timeout_s;
+}
+
+extern "C" int b2_set_spin_timeout(double seconds) {
+  B2_REQUIRE(seconds >= 0.0, B2_ERR_INVALID, "timeout must be >= 0 seconds (0 = wait forever)");
+  g_spin_timeout_s = seconds;
+  return B2_OK;
+}
+
+extern "C" double b2_get_spin_timeout(void) { return spin_timeout_s(); }
 
 extern "C" size_t b2_p2p_flag_bytes(void) { return sizeof(uint32_t) * 2 * kMaxRanks * kMaxSegs; }
 
@@ -550,6 +579,7 @@ static int clip_allreduce_impl(const void* in, void* const* stages, void* mc_sta
   f.rank = rank;
   f.inv_n = 1.0f / (float)nranks;
   f.mc = static_cast<__nv_bfloat16*>(mc_stage);
+  f.timeout_ns = (uint64_t)(spin_timeout_s() * 1e9);
 
   // roles: comm CTAs on the first `cs` SMs (B2_COMM_SMS overrides), clip CTAs
   // on the rest.  Sweeps (profiles/r01_k4_split_sweep.jsonl): P2P best at 64

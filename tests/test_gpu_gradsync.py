@@ -121,10 +121,12 @@ def test_allreduce_kats():
     with pytest.raises(ValueError, match="mismatch|matrix"):
         allreduce_mean([[1.0, 2.0], [3.0]])
     rng = np.random.default_rng(0)
-    for k in (1, 2, 3, 5, 8, 16):
+    for k in (1, 2, 3, 5, 8, 16, 63, 64, 65, 100, 257):
         w = rng.normal(size=(k, 33))
-        # the pairwise tree is the reference's: bit-identical to the oracle
+        # the pairwise tree is the reference's: bit-identical to the oracle, for any K
         np.testing.assert_array_equal(allreduce_mean(w), O.allreduce_mean(w))
+    w = rng.normal(size=(130, 1000))  # > 64 workers through sync_bucketwise (no K cap)
+    np.testing.assert_array_equal(sync_bucketwise(state(w, 3), BUCKET), O.sync_bucketwise(w, equal_bucket_layout(1000, 3), 1.0))
 
 
 def test_bucketwise_kats():

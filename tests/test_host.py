@@ -27,7 +27,8 @@ def header_symbols():
 def test_library_exports_header_symbols():
     lib = _lib.load(require_device=False)
     syms = header_symbols()
-    assert len(syms) == 30, syms
+    assert len(syms) == 34, syms
+    assert set(syms) == set(_lib.SIGNATURES), set(syms) ^ set(_lib.SIGNATURES)
     for s in syms:
         assert hasattr(lib, s), s
         assert s in _lib.SIGNATURES, s
@@ -54,6 +55,22 @@ def test_argument_errors_without_device():
     assert rc == _lib.B2_ERR_INVALID
     rc = lib.b2_weighted_mean(None, 0, 1, 1, 1, None, None, 1, None, 0, None)
     assert rc == _lib.B2_ERR_INVALID
+    rc = lib.b2_presort_sort_deal(None, None, 1, 10000, 3, 1, 512, 10, None, None, None, None, None, 0, None)
+    assert rc == _lib.B2_ERR_INDIVISIBLE
+    # the device-wide sort's scratch: keys x2, histograms, look-back words (1.25M-sample shard)
+    ws = lib.b2_presort_workspace_bytes(1, 1_250_000, 512, 1_249_999, 0)
+    assert 2 * 8 * 1_250_000 < ws < 40 * 1_250_000
+    assert lib.b2_presort_workspace_bytes(1, 4096, 512, 100, 0) == 0  # K3-sized pools need none
+
+
+def test_spin_timeout_setting():
+    """Cross-GPU waits of the fused kernels: configurable bound, 0 = wait forever."""
+    lib = _lib.load(require_device=False)
+    old = lib.b2_get_spin_timeout()
+    assert old >= 0
+    assert lib.b2_set_spin_timeout(0.0) == _lib.B2_OK and lib.b2_get_spin_timeout() == 0.0
+    assert lib.b2_set_spin_timeout(-1.0) == _lib.B2_ERR_INVALID
+    assert lib.b2_set_spin_timeout(old) == _lib.B2_OK
 
 
 @pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")
