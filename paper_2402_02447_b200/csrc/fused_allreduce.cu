@@ -33,6 +33,7 @@
 
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
@@ -586,21 +587,20 @@ static int clip_allreduce_impl(const void* in, void* const* stages, void* mc_sta
   // of 148 SMs for N = 2, 48 for N = 4 (1.63 vs 1.67-1.70 ms at 64), NVLS at 32.
   // Twice the reduce vectors in flight per thread measured slower for both.
   cudaStream_t st = (cudaStream_t)stream;
-  static int csms = -1;
-  if (csms < 0) {
-    const char* e = getenv("B2_COMM_SMS");
-    csms = e ? atoi(e) : 0;
-  }
+  const char* cse = getenv("B2_COMM_SMS");
+  const int csms = cse ? atoi(cse) : 0;
   const int cs = csms > 0 ? csms : (mc_stage ? 32 : nranks <= 2 ? 64 : 48);
   // each reduce thread keeps UC x RMAX 16 B vectors in flight (32 registers)
   if (mc_stage) return launch_split<192, 320, 8, 4, 8, 1, true>(f, st, cs);
-  static int force8 = -1;  // B2_K4_FORCE_R8=1: the 8-rank build at any N (tests that path on <= 4 GPUs)
-  if (force8 < 0) {
-    const char* e = getenv("B2_K4_FORCE_R8");
-    force8 = e ? atoi(e) : 0;
+  // B2_K4_RMAX=2|4|8 picks the rank-count instantiation (>= nranks), read at
+  // every call: tests run each build at the ranks a box has (1-GPU included)
+  int rmax = nranks <= 2 ? 2 : nranks <= 4 ? 4 : 8;
+  if (const char* e = getenv("B2_K4_RMAX")) {
+    const int want = atoi(e);
+    B2_REQUIRE(want == 2 || want == 4 || want == 8, B2_ERR_INVALID, "B2_K4_RMAX must be 2, 4 or 8");
+    rmax = std::max(rmax, want);
   }
-  if (force8) return launch_split<192, 320, 8, 4, 1, 8>(f, st, cs);
-  if (nranks <= 2) return launch_split<192, 320, 8, 4, 4, 2>(f, st, cs);
-  if (nranks <= 4) return launch_split<192, 320, 8, 4, 2, 4>(f, st, cs);
+  if (rmax == 2) return launch_split<192, 320, 8, 4, 4, 2>(f, st, cs);
+  if (rmax == 4) return launch_split<192, 320, 8, 4, 2, 4>(f, st, cs);
   return launch_split<192, 320, 8, 4, 1, 8>(f, st, cs);
 }

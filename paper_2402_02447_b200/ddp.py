@@ -121,6 +121,7 @@ class BucketwiseSync:
             self._offs = _lib.i64_array(self.layout[b][0] for b in order)
             self._lens = _lib.i64_array(self.layout[b][1] - self.layout[b][0] for b in order)
             self._norms_call = torch.zeros(len(self.layout), dtype=torch.float64, device=self.device)
+            self._nonfinite = torch.zeros(len(self.layout), dtype=torch.int32, device=self.device)
             self._pending = False
 
     def sync_native(self, grad: torch.Tensor, stream=None) -> torch.Tensor:
@@ -131,7 +132,8 @@ class BucketwiseSync:
         self.side.wait_stream(s)  # the comm stream must not run ahead of the previous step's readers
         _lib.check(lib.b2_bucket_clip_allreduce(
             self.nccl.handle, grad.data_ptr(), _DT[grad.dtype], self.comm.data_ptr(), _DT[self.comm.dtype],
-            self._offs, self._lens, len(self.layout), float(self.limit), self._norms_call.data_ptr(), None,
+            self._offs, self._lens, len(self.layout), float(self.limit), self._norms_call.data_ptr(),
+            self._nonfinite.data_ptr(),
             ws.data_ptr(), ws.numel(), int(s.cuda_stream), int(self.side.cuda_stream)))
         self._pending = True
         return self.comm
@@ -160,6 +162,20 @@ class BucketwiseSync:
         for b in reversed(range(len(self.layout))):
             self.launch_bucket(grad, b)
         return self.comm
+
+    def check_finite(self) -> None:
+        """Raise the reference's ValueError if any rank's gradient held inf/nan (gradsync.py:111-112).
+
+        Each rank's K1 flags its own non-finite buckets; one small MAX
+        all-reduce of the flags (nseg int32) makes the verdict global.
+        """
+        if not self.native:
+            raise ValueError("non-finite flags are kept by the native path only")
+        flags = self._nonfinite.clone()
+        dist.all_reduce(flags, op=dist.ReduceOp.MAX, group=self.group)
+        if bool(flags.any()):
+            b = len(self.layout) - 1 - int(torch.nonzero(flags)[0])  # call order is reversed bucket order
+            raise ValueError(f"gradient has non-finite components (bucket {b}, on some rank)")
 
     def wait(self) -> torch.Tensor:
         """Join the side stream into the current stream (no host block for NCCL)."""
@@ -260,12 +276,18 @@ class FusedBucketSync:
         self._opened = []
         self.mc = 0
         if transport == "nvls":
+            ok = True
             try:
                 self._setup_nvls(group, stage_bytes, flag_bytes)
             except Exception:
                 if not auto:
                     raise
-                transport = "p2p"  # no multicast here: two-shot over peer memory
+                ok = False
+            if auto:  # every rank must pick the same transport: agree on the outcome (MIN over ranks)
+                flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=self.device)
+                dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+                if int(flag.item()) == 0:
+                    transport, self.mc = "p2p", 0  # no multicast somewhere: two-shot over peer memory
         self.transport = transport
         if transport == "nvls":
             stages = [int(x) for x in self._symm.buffer_ptrs]
@@ -302,6 +324,7 @@ class FusedBucketSync:
             self._chunks.append((c0, len(part), _lib.i64_array(self.layout[b][0] for b in part),
                                  _lib.i64_array(self.layout[b][1] - self.layout[b][0] for b in part)))
         self._norms_call = torch.zeros(len(self.layout), dtype=torch.float64, device=self.device)
+        self._starts = torch.tensor([a for a, _ in self.layout], dtype=torch.int64, device=self.device)
         torch.cuda.synchronize(self.device)
         dist.barrier(group=group)
 
@@ -380,7 +403,26 @@ class FusedBucketSync:
                 out[a:b].copy_(self.stage[a:b], non_blocking=True)
         compute.wait_stream(self._d2h)
         compute.synchronize()
+        self.check_finite()
         return out
+
+    def nonfinite_buckets(self) -> torch.Tensor:
+        """Per bucket (layout order, device bool): did ANY rank's bucket hold inf/nan?
+
+        The reference rejects non-finite gradients (gradsync.py:111-112,
+        189-190).  K4 stages a non-finite bucket as all-NaN, so after the
+        mean the whole bucket is NaN on every rank and one element per bucket
+        tells, locally, whether any rank had one (no extra collective, no
+        host sync; stream-ordered after ``sync``).
+        """
+        return torch.isnan(self.stage.index_select(0, self._starts))
+
+    def check_finite(self) -> None:
+        """Raise the reference's ValueError if any rank's gradient was non-finite (host sync)."""
+        bad = self.nonfinite_buckets()
+        if bool(bad.any()):
+            b = int(torch.nonzero(bad)[0])
+            raise ValueError(f"gradient has non-finite components (bucket {b}, on some rank)")
 
     def _host_chunks(self, chunk_buckets: int):
         cache = getattr(self, "_hchunks", {})

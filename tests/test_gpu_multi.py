@@ -1,6 +1,10 @@
-"""H1 over NCCL on >= 2 GPUs: per-bucket K1 + ncclAllReduce(avg) == reference semantics.
+"""H1/H2 across ranks (one process per GPU, NCCL) == reference semantics.
 
-Skipped on single-GPU boxes; run with `gpurun --gpus 2`.
+Runs at world = min(#GPUs, 4): on a 1-GPU box every test still runs at
+world size 1, so the multi-rank code paths (NCCL communicator, K4's role
+split, flags, epochs and graph replay, the DDP hook, LocalPresort) are
+exercised by the single-GPU suite too; `gpurun --gpus 2|4` runs them across
+ranks.
 """
 
 import numpy as np
@@ -19,7 +23,7 @@ LAYOUT8 = ((0, 6_553_600), (6_553_600, 13_107_200), (13_107_200, 19_660_800), (1
 
 
 def _world():
-    return min(torch.cuda.device_count(), 4)
+    return max(1, min(torch.cuda.device_count(), 4))
 
 
 def _sync_worker(rank, world, port, q):
@@ -117,7 +121,6 @@ def _run(target, world):
     return res
 
 
-@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
 def test_bucketwise_sync_nccl_matches_reference():
     from oracle import ddp_oracle as O
 
@@ -135,7 +138,6 @@ def test_bucketwise_sync_nccl_matches_reference():
         np.testing.assert_allclose(res[r]["norms"], rn, rtol=1e-6)
 
 
-@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
 def test_ddp_comm_hook_nccl():
     from oracle import ddp_oracle as O
 
@@ -147,7 +149,6 @@ def test_ddp_comm_hook_nccl():
         assert np.abs(res[r]["synced"] - ref).max() <= 1e-5 * np.abs(ref).max()
 
 
-@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
 def test_fused_clip_allreduce_p2p_matches_reference():
     from oracle import ddp_oracle as O
 
@@ -187,7 +188,6 @@ def _presort_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
 def test_local_presort_nccl_matches_reference():
     from oracle import ddp_oracle as O
 
@@ -205,15 +205,21 @@ def test_local_presort_nccl_matches_reference():
 
 
 def _fused_nvls_worker(rank, world, port, q):
-    _fused_worker(rank, world, port, q, transport="nvls")
+    try:
+        _fused_worker(rank, world, port, q, transport="nvls")
+    except RuntimeError as e:
+        if "multicast" not in str(e):
+            raise
+        q.put((rank, {"skip": str(e)}))
 
 
-@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
 def test_fused_clip_allreduce_nvls_matches_reference():
     from oracle import ddp_oracle as O
 
     world = _world()
     res = _run(_fused_nvls_worker, world)
+    if any("skip" in res[r] for r in range(world)):
+        pytest.skip(res[0].get("skip", "no multicast"))
     W = np.stack([H.worker_grad(r, DIM8).double().numpy() for r in range(world)])
     ref = O.sync_bucketwise(W, LAYOUT8, 1.0)
     scale = np.abs(ref).max()
@@ -255,7 +261,6 @@ def _hook_multi_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
 def test_ddp_comm_hook_multi_bucket_nccl():
     """DDP with several buckets: every parameter gradient equals mean_r clip(bucket_r, c/sqrt(B))."""
     from oracle import ddp_oracle as O
@@ -301,7 +306,6 @@ def _fused_large_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
 def test_fused_bert_large_streamed_equals_device_and_oracle():
     """BERT-large (52 x 25 MiB): sync_host (H2D / K4 / D2H per chunk) == sync (device),
     bit for bit, identical on every rank, and within bf16 of the oracle on sampled buckets."""
