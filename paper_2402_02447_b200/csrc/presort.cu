@@ -168,124 +168,246 @@ __global__ void __launch_bounds__(32 * WARPS) k_presort_deal_warp(const __grid_c
   }
 }
 
-// Warp-per-pool COUNTING sort (lengths are small integers): histogram of the
-// pool's lengths in shared memory (the atomic's return value ranks each key
-// inside its bin), one warp scan over the bins, a scatter into sorted order,
-// then ids ordered inside each multi-key bin (equal lengths; a handful of
-// keys on real data).  O(pool) work instead of the bitonic network's
-// O(pool log^2 pool) 64-bit compare-exchanges; (-len, id) is unique per
-// sample, so the output is the same.  Pools <= 512 keys, lengths <= 1024.
-constexpr int kCntBins = 1024;
-constexpr int kCntMaxSeg = 512;
+// Warp-per-pool COUNTING sort (lengths are small integers), sized for
+// occupancy (~2.8 KB of shared memory per warp, two registers per key).
+// Per pool:
+//   1. length histogram, two 16-bit bins per word; the packed atomic's old
+//      value ranks each key inside its bin (bin 0 = longest);
+//   2. one warp scan turns the packed counts into packed bin starts;
+//   3. each id is scattered to start+rank of its bin.  Every key of a bin has
+//      the same length, so the bin's contribution to each GPU lane's token sum
+//      (_from_per_gpu, balance.py:54-56) is fixed by the bin's slots alone and
+//      is added here, before the order inside the bin is known;
+//   4. each bin is put in id order (the reference's (-len, id) key,
+//      balance.py:73-75): bins of 2+ keys are listed by their second key and
+//      insertion-sorted in place, one lane per bin (bins hold ~1 key on real
+//      data); bins above kCntBig keys are ranked by the whole warp instead.  Equal (len, id) pairs are identical
+//      samples, so their order is immaterial;
+//   5. the deal is a GATHER: output slot o = lane*rows + r reads sorted
+//      position r*lanes + c (c mirrored on odd rows for SNAKE,
+//      balance.py:59-70), so the [lanes][rows] tile is written with
+//      consecutive addresses and no staging buffer.
+// The next pool's lines are prefetched into L2 while this one is sorted.
+// Input order inside a pool is irrelevant to the result, so VEC loads 4
+// consecutive keys per lane.
+constexpr int kCntWarps = 4;
+constexpr int kCntBins = 1024;   // max_len limit of the counting path
+constexpr int kCntMaxSeg = 512;  // pool limit of the counting path
+constexpr int kCntTok = 64;      // lanes whose token sums stay in shared memory (more: global atomics)
+constexpr int kCntBig = 24;      // bins above this many keys are sorted by the whole warp
 
-template <int WARPS>
-__global__ void __launch_bounds__(32 * WARPS) k_presort_deal_count(const __grid_constant__ PresortParams p) {
-  __shared__ int s_hist[WARPS][kCntBins];         // counts, then bin starts
-  __shared__ int32_t s_sid[WARPS][kCntMaxSeg];    // sorted ids
-  __shared__ int16_t s_slen[WARPS][kCntMaxSeg];   // sorted lengths
-  __shared__ int32_t s_oid[WARPS][kCntMaxSeg];    // dealt [lane][row]
-  __shared__ int16_t s_olen[WARPS][kCntMaxSeg];
-  constexpr int KM = kCntMaxSeg / 32;
+template <int KM, int HW, int MINB, bool VEC>
+__global__ void __launch_bounds__(32 * kCntWarps, MINB) k_presort_deal_count(const __grid_constant__ PresortParams p) {
+  constexpr int PM = 32 * KM;    // pool capacity
+  constexpr int WPL = HW / 32;   // histogram words per lane in the scan (2 bins each)
+  __shared__ __align__(16) uint32_t s_hist[kCntWarps][HW];  // packed counts, then packed starts
+  __shared__ int32_t s_srt[kCntWarps][PM];                  // ids grouped by bin, then sorted
+  __shared__ int32_t s_tok[kCntWarps][kCntTok];             // per-lane token sums
+  __shared__ int16_t s_mul[kCntWarps][PM / 2];              // bins with 2+ keys; big bins from the top
+  __shared__ int s_cnt[kCntWarps][2];                       // list lengths
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int M = p.max_len, P = p.seg_len;
-  const int per = (M + 31) / 32;  // bins per lane in the scan
-  int* hist = s_hist[w];
-  const int64_t nwarps = (int64_t)gridDim.x * WARPS;
-  for (int64_t seg = (int64_t)blockIdx.x * WARPS + w; seg < p.nseg; seg += nwarps) {
+  const int M = p.max_len, P = p.seg_len, rows = p.rows, lanes = p.lanes;
+  uint32_t* hist = s_hist[w];
+  int32_t* srt = s_srt[w];
+  int32_t* stok = s_tok[w];
+  int16_t* smul = s_mul[w];
+  const bool tok_smem = lanes <= kCntTok;
+  const float inv_lanes = 1.0f / (float)lanes;
+  const int ln0 = lane / rows, r0 = lane - ln0 * rows;  // deal coordinates of output slot `lane`
+  const int dq = 32 / rows, dr = 32 - dq * rows;        // ... and their step per 32 slots
+  const int64_t nwarps = (int64_t)gridDim.x * kCntWarps;
+  for (int k = lane; k < kCntTok; k += 32) stok[k] = 0;
+  if (lane < 2) s_cnt[w][lane] = 0;
+  __syncwarp();
+  for (int64_t seg = (int64_t)blockIdx.x * kCntWarps + w; seg < p.nseg; seg += nwarps) {
     const int64_t base = seg * P;
-    for (int b = lane; b < M; b += 32) hist[b] = 0;
-    __syncwarp();
-    int32_t id[KM];
-    int16_t len[KM], rk[KM];
-    long long first_bad = -1;
+    if (seg + nwarps < p.nseg) {  // next pool of this warp -> L2
+      const int64_t nb = base + nwarps * P;
+      const int nl = (P * 4 + 127) / 128 + 1;
+      for (int k = lane; k < 2 * nl; k += 32) {
+        const int32_t* a0 = (k < nl ? p.lens : p.ids) + nb;
+        const int32_t* a = a0 + (int64_t)(k < nl ? k : k - nl) * 32;
+        if (a < a0 + P) asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+      }
+    }
 #pragma unroll
-    for (int j = 0; j < KM; ++j) {
-      const int i = j * 32 + lane;  // striped: coalesced loads
-      if (i < P) {
-        int32_t L = p.lens[base + i];
-        const int32_t D = p.ids[base + i];
-        if (!(L >= 1 && L <= M && D >= 0 && D <= p.max_id)) {
-          if (first_bad < 0) first_bad = base + i;
-          L = L < 1 ? 1 : (L > M ? M : L);  // keep the slot well-formed; the caller raises
+    for (int k = lane; k < HW / 4; k += 32) reinterpret_cast<uint4*>(hist)[k] = make_uint4(0, 0, 0, 0);
+    if (!tok_smem && p.tokens)
+      for (int k = lane; k < lanes; k += 32) p.tokens[seg * lanes + k] = 0;
+    __syncwarp();
+    uint32_t kb[KM];  // (bin << 16) | rank in bin
+    int32_t kd[KM];   // ids
+    long long first_bad = -1;
+    auto add_key = [&](int j, int64_t flat, int32_t L, int32_t D) {
+      if (!(L >= 1 && L <= M && D >= 0 && D <= p.max_id)) {
+        if (first_bad < 0 || flat < first_bad) first_bad = flat;
+        L = L < 1 ? 1 : (L > M ? M : L);  // keep the slot well-formed; the caller raises
+      }
+      const uint32_t bin = (uint32_t)(M - L), sh = (bin & 1u) << 4;
+      const uint32_t old = atomicAdd(&hist[bin >> 1], 1u << sh);
+      kb[j] = (bin << 16) | ((old >> sh) & 0xffffu);
+      kd[j] = D;
+    };
+    auto live = [&](int j) { return VEC ? ((j / 4) * 32 + lane) * 4 < P : j * 32 + lane < P; };
+    if constexpr (VEC) {
+#pragma unroll
+      for (int j4 = 0; j4 < KM / 4; ++j4) {
+        const int i = (j4 * 32 + lane) * 4;
+        if (i < P) {
+          const int4 L4 = __ldg(reinterpret_cast<const int4*>(p.lens + base + i));
+          const int4 D4 = __ldg(reinterpret_cast<const int4*>(p.ids + base + i));
+          add_key(4 * j4 + 0, base + i + 0, L4.x, D4.x);
+          add_key(4 * j4 + 1, base + i + 1, L4.y, D4.y);
+          add_key(4 * j4 + 2, base + i + 2, L4.z, D4.z);
+          add_key(4 * j4 + 3, base + i + 3, L4.w, D4.w);
         }
-        id[j] = D;
-        len[j] = (int16_t)L;
-        rk[j] = (int16_t)atomicAdd(&hist[M - L], 1);  // bin 0 = longest
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < KM; ++j) {
+        const int i = j * 32 + lane;  // striped: coalesced loads
+        if (i < P) add_key(j, base + i, __ldg(p.lens + base + i), __ldg(p.ids + base + i));
       }
     }
     if (first_bad >= 0 && p.bad) atomicMin(reinterpret_cast<unsigned long long*>(p.bad), (unsigned long long)first_bad);
     __syncwarp();
-    {  // exclusive scan over the M bins: `per` contiguous bins per lane
-      const int b0 = lane * per, b1 = min(b0 + per, M);
-      int sum = 0;
-      for (int b = b0; b < b1; ++b) sum += hist[b];
-      int inc = sum;
+    {  // packed exclusive scan: lane owns WPL consecutive words = bins [2*WPL*lane, 2*WPL*(lane+1))
+      uint32_t v[WPL];
+#pragma unroll
+      for (int k = 0; k < WPL / 4; ++k) {
+        const uint4 q = reinterpret_cast<const uint4*>(hist)[lane * (WPL / 4) + k];
+        v[4 * k] = q.x, v[4 * k + 1] = q.y, v[4 * k + 2] = q.z, v[4 * k + 3] = q.w;
+      }
+      uint32_t tot = 0;
+#pragma unroll
+      for (int k = 0; k < WPL; ++k) tot += (v[k] & 0xffffu) + (v[k] >> 16);
+      uint32_t inc = tot;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, inc, o);
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
         if (lane >= o) inc += y;
       }
-      int ex = inc - sum;
-      for (int b = b0; b < b1; ++b) {
-        const int c = hist[b];
-        hist[b] = ex;
-        ex += c;
-      }
-    }
-    __syncwarp();
+      uint32_t ex = inc - tot;
 #pragma unroll
-    for (int j = 0; j < KM; ++j) {
-      const int i = j * 32 + lane;
-      if (i < P) {
-        const int pos = hist[M - len[j]] + rk[j];
-        s_sid[w][pos] = id[j];
-        s_slen[w][pos] = len[j];
+      for (int k = 0; k < WPL; ++k) {
+        const uint32_t lo = v[k] & 0xffffu, hi = v[k] >> 16;
+        v[k] = ex | ((ex + lo) << 16);
+        ex += lo + hi;
       }
+#pragma unroll
+      for (int k = 0; k < WPL / 4; ++k)
+        reinterpret_cast<uint4*>(hist)[lane * (WPL / 4) + k] = make_uint4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
     }
     __syncwarp();
-    {  // equal lengths: ids ascending inside each bin (insertion sort; bins are tiny)
-      const int b0 = lane * per, b1 = min(b0 + per, M);
-      for (int b = b0; b < b1; ++b) {
-        const int st = hist[b], en = b + 1 < M ? hist[b + 1] : P;
-        for (int x = st + 1; x < en; ++x) {
-          const int32_t v = s_sid[w][x];
-          int y = x - 1;
-          while (y >= st && s_sid[w][y] > v) {
-            s_sid[w][y + 1] = s_sid[w][y];
-            --y;
-          }
-          s_sid[w][y + 1] = v;
+    int32_t* out = p.out_ids + base;
+#pragma unroll
+    for (int j = 0; j < KM; ++j) {  // ids into their bins; the bin's slots fix its token shares
+      if (live(j)) {
+        const uint32_t bin = kb[j] >> 16, rk = kb[j] & 0xffffu;
+        const int pos = (int)(((hist[bin >> 1] >> ((bin & 1u) << 4)) & 0xffffu) + rk);
+        srt[pos] = kd[j];
+        if (rk == 1) smul[atomicAdd(&s_cnt[w][0], 1)] = (int16_t)bin;  // the bin holds 2+ keys
+        if (p.tokens) {  // the GPU lane slot `pos` is dealt to
+          const int r = __float2int_rd(((float)pos + 0.5f) * inv_lanes), c = pos - r * lanes;
+          const int g = (p.snake && (r & 1)) ? lanes - 1 - c : c;
+          const int L = M - (int)bin;
+          if (tok_smem) atomicAdd(&stok[g], L);
+          else atomicAdd(reinterpret_cast<unsigned long long*>(p.tokens + seg * lanes + g), (unsigned long long)L);
         }
       }
     }
     __syncwarp();
-    for (int q = lane; q < P; q += 32) {  // deal (balance.py:59-70)
-      const int r = q / p.lanes, c = q - r * p.lanes;
-      const int ln = (p.snake && (r & 1)) ? p.lanes - 1 - c : c;
-      s_oid[w][ln * p.rows + r] = s_sid[w][q];
-      s_olen[w][ln * p.rows + r] = s_slen[w][q];
+    // bins with 2+ keys (listed by their second key in the scatter) are put in id order,
+    // spread over the lanes; bins above kCntBig keys go to a second list for the whole warp
+    const int nmulti = s_cnt[w][0];
+    auto bstart = [&](int b) { return b < M ? (int)((hist[b >> 1] >> ((b & 1) << 4)) & 0xffffu) : P; };
+    for (int q = lane; q < nmulti; q += 32) {
+      const int b = smul[q], st = bstart(b), e = bstart(b + 1);
+      if (e - st > kCntBig) {
+        smul[PM / 2 - 1 - atomicAdd(&s_cnt[w][1], 1)] = (int16_t)b;  // big list grows from the top
+        continue;
+      }
+      for (int x = st + 1; x < e; ++x) {  // insertion sort, ids ascending
+        const int32_t val = srt[x];
+        int y = x - 1;
+        int32_t prev = srt[y];
+        while (prev > val) {
+          srt[y + 1] = prev;
+          if (--y < st) break;
+          prev = srt[y];
+        }
+        srt[y + 1] = val;
+      }
     }
     __syncwarp();
-    int32_t* out = p.out_ids + base;
-    for (int i = lane; i < P; i += 32) out[i] = s_oid[w][i];
-    if (p.tokens)
-      for (int l = lane; l < p.lanes; l += 32) {
-        int64_t sum = 0;  // per-lane token sum (_from_per_gpu, balance.py:54-56)
-        for (int r = 0; r < p.rows; ++r) sum += s_olen[w][l * p.rows + r];
-        p.tokens[seg * p.lanes + l] = sum;
+    const int nbig = s_cnt[w][1];
+    for (int q = 0; q < nbig; ++q) {
+      // rank every element by (id, slot) against the bin; stage the sorted bin in this pool's
+      // own output rows (global, rewritten by the gather below)
+      const int b = smul[PM / 2 - 1 - q], st = bstart(b), e = bstart(b + 1);
+      for (int x = st + lane; x < e; x += 32) {
+        const int32_t me = srt[x];
+        int f = st;
+        for (int y = st; y < e; ++y) {
+          const int32_t o = srt[y];
+          f += (o < me) || (o == me && y < x);
+        }
+        out[f] = me;
       }
+      __syncwarp();
+      for (int x = st + lane; x < e; x += 32) srt[x] = out[x];
+      __syncwarp();
+    }
+    if (lane == 0) s_cnt[w][0] = s_cnt[w][1] = 0;
     __syncwarp();
+    int ln = ln0, r = r0;
+#pragma unroll 4
+    for (int o = lane; o < P; o += 32) {  // the deal as a gather (balance.py:59-70)
+      const int c = (p.snake && (r & 1)) ? lanes - 1 - ln : ln;
+      out[o] = srt[r * lanes + c];
+      r += dr;
+      ln += dq;
+      if (r >= rows) {
+        r -= rows;
+        ++ln;
+      }
+    }
+    if (tok_smem && p.tokens) {
+      __syncwarp();
+      for (int k = lane; k < lanes; k += 32) {
+        p.tokens[seg * lanes + k] = stok[k];
+        stok[k] = 0;
+      }
+    }
+    __syncwarp();  // shared buffers are reused by the next pool
   }
 }
 
-template <int WARPS>
+template <int KM, int HW>
 int launch_count(const PresortParams& p, cudaStream_t st) {
+  // CTAs per SM from the shared-memory footprint (+1 KB reserved per CTA)
+  constexpr int kSmem = kCntWarps * (HW * 4 + 32 * KM * 5 + kCntTok * 4 + 8);
+  // and registers: 64 per thread (8 CTAs) keeps the unrolled loads spill-free;
+  // the 256-bin pools up to 384 keys fit 48 (10 CTAs)
+  constexpr int kRegB = 8;
+  constexpr int kSmemB = (220 * 1024) / (kSmem + 1024);
+  constexpr int kMinB = kSmemB < kRegB ? kSmemB : kRegB;
   const DeviceInfo& di = device_info();
-  const int64_t blocks = (p.nseg + WARPS - 1) / WARPS;
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)di.sm_count * 16));
-  k_presort_deal_count<WARPS><<<grid, 32 * WARPS, 0, st>>>(p);
+  const int64_t blocks = (p.nseg + kCntWarps - 1) / kCntWarps;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)di.sm_count * kMinB));
+  const bool vec = KM % 4 == 0 && p.seg_len % 4 == 0 && ((uintptr_t)p.ids & 15) == 0 && ((uintptr_t)p.lens & 15) == 0;
+  if (vec) k_presort_deal_count<KM, HW, kMinB, true><<<grid, 32 * kCntWarps, 0, st>>>(p);
+  else k_presort_deal_count<KM, HW, kMinB, false><<<grid, 32 * kCntWarps, 0, st>>>(p);
   B2_CHECK(cudaGetLastError());
   return B2_OK;
+}
+
+template <int HW>
+int launch_count_km(const PresortParams& p, cudaStream_t st) {
+  if (p.seg_len <= 128) return launch_count<4, HW>(p, st);
+  if (p.seg_len <= 256) return launch_count<8, HW>(p, st);
+  if (p.seg_len <= 384) return launch_count<12, HW>(p, st);
+  return launch_count<16, HW>(p, st);
 }
 
 template <int K, int WARPS>
@@ -350,16 +472,16 @@ extern "C" int b2_presort_deal(const int32_t* ids, const int32_t* lens, int64_t 
   p.tokens = tokens;
   p.bad = bad;
   B2_REQUIRE(p.end_bit <= 64, B2_ERR_UNSUPPORTED, "key does not fit 64 bits");
-  static int variant = -1;  // B2_PRESORT_PATH=bitonic forces the network (A/B runs, tests)
+  // B2_PRESORT_PATH=bitonic|count forces one warp path (A/B runs, tests)
+  static int variant = -1;
   if (variant < 0) {
     const char* e = getenv("B2_PRESORT_PATH");
-    variant = (e && !strcmp(e, "bitonic")) ? 1 : 0;
+    variant = (e && !strcmp(e, "bitonic")) ? 1 : (e && !strcmp(e, "count")) ? 2 : 0;
   }
-  // counting sort pays when the pool fills at least half of the length bins
-  // (lb48: 384 keys / 512 bins, 1.37x over the network); smaller pools sort
-  // faster in registers than the bins can be cleared and scanned (lb16: 3x)
-  if (!out_pos && variant == 0 && seg_len <= kCntMaxSeg && max_len <= kCntBins && 2 * seg_len >= max_len)
-    return launch_count<4>(p, st);
+  const bool count_ok = !out_pos && seg_len <= kCntMaxSeg && max_len <= kCntBins;
+  // counting sort pays when the pool is not tiny next to the length bins
+  if (count_ok && (variant == 2 || (variant == 0 && 4 * seg_len >= max_len)))
+    return max_len <= 512 ? launch_count_km<256>(p, st) : launch_count_km<512>(p, st);
   if (!out_pos) {  // no input slots needed: warp-per-pool bitonic network
     if (seg_len <= 64) return launch_warp<2, 8>(p, st);
     if (seg_len <= 128) return launch_warp<4, 8>(p, st);

@@ -355,3 +355,46 @@ def test_strategy_properties_conservation_and_snake():
         raster = assign_global_presort(samples, Topology(1, gpus), "raster")
         snake = assign_global_presort(samples, Topology(1, gpus), "snake")
         assert max(snake.token_counts) - min(snake.token_counts) <= max(raster.token_counts) - min(raster.token_counts)
+
+
+@pytest.mark.parametrize("max_len", [64, 512, 1000])
+@pytest.mark.parametrize("seg_len,lanes", [(32, 8), (128, 8), (200, 8), (256, 256), (384, 8), (384, 1), (480, 3),
+                                           (512, 16)])
+def test_counting_path_every_instantiation(seg_len, lanes, max_len):
+    """The warp counting-sort path (b2_presort_deal when 4 * pool >= max_len, max_len <= 1024) in
+    every (keys per lane, histogram words) instantiation, one row per lane up to one lane per
+    key, raster and snake, with repeated samples (same id, same length) and runs of equal
+    lengths: equal to the oracle (balance.py:59-75)."""
+    rng = np.random.default_rng(seg_len * 31 + lanes + max_len)
+    nseg = 257
+    ids = rng.integers(0, 5 * seg_len, size=(nseg, seg_len)).astype(np.int32)  # repeats inside a pool
+    lens = rng.integers(1, max_len + 1, size=(nseg, seg_len)).astype(np.int32)
+    lens[::3, : seg_len // 2] = rng.integers(max(1, max_len - 3), max_len + 1, size=(len(lens[::3]), seg_len // 2))
+    lens[ids % 7 == 0] = 1 + ids[ids % 7 == 0] % max_len  # repeated ids -> identical samples
+    di, dl = torch.from_numpy(ids.reshape(-1)).cuda(), torch.from_numpy(lens.reshape(-1)).cuda()
+    for scan in ("raster", "snake"):
+        out, tok, _, bad = presort_deal(di, dl, seg_len, lanes, scan, max_len=max_len, max_id=5 * seg_len)
+        assert int(bad) == -1
+        ro, rt = O.presort_deal_segments(ids.reshape(-1), lens.reshape(-1), seg_len, lanes, scan == "snake")
+        np.testing.assert_array_equal(out.cpu().numpy(), ro)
+        np.testing.assert_array_equal(tok.cpu().numpy(), rt)
+
+
+def test_counting_path_all_equal_lengths_and_bad_keys():
+    """Worst case for the in-bin id ordering (every key in one bin), and the first bad key
+    (length 0 / above max_len / negative id) reported as the flat index, as before."""
+    seg_len, lanes, nseg = 384, 8, 40
+    rng = np.random.default_rng(5)
+    ids = np.stack([rng.permutation(100_000)[:seg_len] for _ in range(nseg)]).astype(np.int32)
+    lens = np.full((nseg, seg_len), 77, dtype=np.int32)
+    di, dl = torch.from_numpy(ids.reshape(-1)).cuda(), torch.from_numpy(lens.reshape(-1)).cuda()
+    out, tok, _, bad = presort_deal(di, dl, seg_len, lanes, "snake", max_len=512, max_id=100_000)
+    ro, rt = O.presort_deal_segments(ids.reshape(-1), lens.reshape(-1), seg_len, lanes, True)
+    np.testing.assert_array_equal(out.cpu().numpy(), ro)
+    np.testing.assert_array_equal(tok.cpu().numpy(), rt)
+    for flat, field, val in ((5000, "len", 0), (1234, "len", 513), (9000, "id", -3)):
+        l2, i2 = lens.reshape(-1).copy(), ids.reshape(-1).copy()
+        (l2 if field == "len" else i2)[flat] = val
+        r = presort_deal(torch.from_numpy(i2).cuda(), torch.from_numpy(l2).cuda(), seg_len, lanes, "snake",
+                         max_len=512, max_id=100_000)
+        assert int(r[3]) == flat
