@@ -10,7 +10,10 @@ import ctypes as C
 import threading
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "_native" / "libb2ddp.so"
+import os
+
+# B2_LIB_PATH: load another build of the same library (A/B measurements under tools/)
+LIB_PATH = Path(os.environ.get("B2_LIB_PATH") or Path(__file__).resolve().parent / "_native" / "libb2ddp.so")
 
 B2_OK, B2_ERR_INVALID, B2_ERR_CUDA, B2_ERR_INDIVISIBLE, B2_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 B2_F32, B2_BF16, B2_F64 = 0, 1, 2
