@@ -4,23 +4,28 @@
 // searchsorted(bounds, length, side='left') (:74), samples are appended to
 // their stratum in input order (:81), probs = count/N (:82; host side).
 //
-// Two launches for ALL rank shards at once (HBM/L2-streaming, 8 B/key
-// algorithmic: 4 B length read, 4 B id written; +4 B if explicit ids are read):
-//   k_strata_count  : one CTA per 4096-key tile -> per-tile per-stratum counts
-//                     (striped loads, #{len > bound} per bound, differenced;
-//                     + the shard's first bad index via atomicMin)
-//                     and, in the LAST tile of each shard to finish (atomic
-//                     ticket), the shard's exclusive per-tile prefixes (in
-//                     place over the tile counts) and per-stratum totals —
-//                     no scan launch, no O(tiles^2) re-summing
-//   k_strata_scatter: one CTA per tile reads its prefix row + the shard totals,
-//                     then places its keys with stable in-tile ranks from a
-//                     single packed block scan (4 strata x 16-bit fields per
-//                     u64), staged through shared memory so each stratum's run
-//                     is written with consecutive addresses.
+// Two launches for ALL rank shards at once.  Algorithmic traffic is 8 B/key
+// (4 B length read, 4 B id written; +4 B if explicit ids are read); the
+// launches move 8.5 B/key (2-bit stratum codes, 4-bit above 4 strata):
+//   k_strata_count  : one CTA per 4096-key tile reads the lengths once (16 B
+//                     vector loads), writes each key's stratum CODE packed 16
+//                     per word (0.25 B/key), counts per tile and stratum, and,
+//                     in the LAST tile of each shard to finish (atomic
+//                     ticket), turns the shard's tile counts into exclusive
+//                     prefixes (in place) and writes the shard totals;
+//   k_strata_scatter: one CTA per tile, one warp per 512 keys, reads only the
+//                     codes: warp counts from the packed words, the tile's
+//                     warps scanned in shared memory, then 16 rounds of 32 keys
+//                     in input order — a key's rank among the round's keys of
+//                     its stratum comes from CB ballots (one per code bit), its
+//                     run base from the lane that owns that stratum (shuffle)
+//                     — and each id is stored straight to its final slot (a
+//                     round writes <= nb contiguous runs: coalesced, no staging).
+// A bad sample (length < 1 or above the last bound) is reported through
+// `bad` (the wrapper raises like the reference); it is placed in the nearest
+// stratum, so ids_out/counts of that shard are unspecified.
 #include "common.cuh"
 
-#include <cub/block/block_load.cuh>
 #include <cub/block/block_scan.cuh>
 
 #include <algorithm>
@@ -30,10 +35,9 @@ namespace {
 
 constexpr int kMaxStrata = 16;
 constexpr int kT = 256;            // threads per tile CTA
-constexpr int kItems = 16;         // keys per thread
-constexpr int kTile = kT * kItems; // 4096 keys per tile (fits 16-bit fields)
-
-constexpr int kMaxShards = 64;  // shards (segments) per launch
+constexpr int kTile = 4096;        // keys per tile (8 warps x 512)
+constexpr int kWarpKeys = 512;     // keys per warp in the scatter
+constexpr int kMaxShards = 64;     // shards (segments) per launch
 
 struct StrataParams {
   const int32_t* len;
@@ -44,102 +48,113 @@ struct StrataParams {
   int32_t tile_off[kMaxShards + 1];   // first tile of each shard
   int32_t* tile_counts;               // [T][kMaxStrata]: counts, then exclusive in-shard prefixes
   unsigned* shard_done;               // [kMaxShards] tiles counted per shard (zeroed per launch)
+  uint32_t* codes;                    // [T][kTile * CB / 32] packed stratum codes
   int64_t* counts;                    // [nshard][nb] totals
   int64_t* bad;                       // [nshard] first bad index within the shard (u64 min), pre-set to -1
   int32_t* ids_out;                   // same offsets as the input
 };
 
 template <int NB>
-__device__ __forceinline__ int stratum_of(int32_t len, const StrataParams& p) {
-  int k = 0;
-#pragma unroll
-  for (int j = 0; j < NB; ++j) k += (len > p.bounds[j]);  // == searchsorted(..., 'left'); unused bounds are INT32_MAX
-  return k;
-}
+__host__ __device__ constexpr int code_bits() { return NB <= 4 ? 2 : 4; }
 
 __device__ __forceinline__ int shard_of_tile(const StrataParams& p, int tile) {
-  int g = 0;
-  while (g + 1 < p.nshard && p.tile_off[g + 1] <= tile) ++g;
-  return g;
+  int lo = 0, hi = p.nshard - 1;  // last g with tile_off[g] <= tile (binary search, <= 6 steps)
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (p.tile_off[mid] <= tile) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
 }
 
-template <int NW>
-struct Packed {
-  unsigned long long w[NW];
-  __device__ __forceinline__ Packed operator+(const Packed& o) const {
-    Packed r;
-#pragma unroll
-    for (int i = 0; i < NW; ++i) r.w[i] = w[i] + o.w[i];
-    return r;
-  }
-  __device__ __forceinline__ unsigned field(int k) const {
-    return (unsigned)((w[k >> 2] >> ((k & 3) * 16)) & 0xffffull);
-  }
-};
-
-using LoadT = cub::BlockLoad<int32_t, kT, kItems, cub::BLOCK_LOAD_WARP_TRANSPOSE>;
-
-// pass 1: per-tile stratum counts (+ first bad sample of the shard).  Order
-// is irrelevant for counting, so keys load striped (direct coalesced loads),
-// and each thread counts #{len > bound_j} per bound with the bounds in
-// registers; stratum counts are differences of those (stratum 0 also drops
-// lengths < 1; lengths beyond the last bound cancel out).  Bad samples only
-// cost a block OR unless one exists.
+// pass 1: codes + per-tile counts (+ the shard's first bad sample), then the
+// shard's last tile scans the tile counts into prefixes.  The code is
+// sum_{q < nb-1} (len > bound_q): a length above the last bound lands in the
+// last stratum and one below 1 in the first, so bad samples need no branch.
 template <int NB>
 __global__ void __launch_bounds__(kT) k_strata_count(const __grid_constant__ StrataParams p) {
-  __shared__ int cnt[kMaxStrata + 1];  // [NB] strata, [NB] = valid keys >= 1
+  constexpr int CB = code_bits<NB>();
+  constexpr int WPT = kTile * CB / 32;   // code words per tile
+  constexpr int QPW = 32 / (4 * CB);     // 4-key quads per word (4 or 2)
+  __shared__ int cnt[kMaxStrata];
   const int tile = blockIdx.x;
   const int g = shard_of_tile(p, tile);
   const int64_t sbeg = p.shard_off[g], send = p.shard_off[g + 1];
   const int64_t lbase = (int64_t)(tile - p.tile_off[g]) * kTile;  // within the shard
   const int valid = (int)min64(kTile, send - sbeg - lbase);
-  if (threadIdx.x <= kMaxStrata) cnt[threadIdx.x] = 0;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x < kMaxStrata) cnt[threadIdx.x] = 0;
   const int32_t* L = p.len + sbeg + lbase;
-  int32_t bnd[NB];
+  const bool vec = (((uintptr_t)L) & 15) == 0 && valid == kTile;
+  int32_t bnd[NB - 1 > 0 ? NB - 1 : 1];
 #pragma unroll
-  for (int q = 0; q < NB; ++q) bnd[q] = p.bounds[q];
-  const int32_t blast = p.bounds[p.nb - 1];
-  int32_t v[kItems];
+  for (int q = 0; q < NB - 1; ++q) bnd[q] = q < p.nb - 1 ? p.bounds[q] : INT32_MAX;
+  const uint32_t blast = (uint32_t)p.bounds[p.nb - 1];
+  // per-thread counts: quads counted from their packed codes
+  int c[NB];
 #pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    const int idx = j * kT + threadIdx.x;
-    v[j] = idx < valid ? L[idx] : 1;  // padding: a length that counts nowhere (fixed below)
+  for (int q = 0; q < NB; ++q) c[q] = 0;
+  bool anybad = false;
+  uint32_t* cw = p.codes + (int64_t)tile * WPT;
+#pragma unroll
+  for (int it = 0; it < kTile / (4 * kT); ++it) {  // 4 consecutive keys per thread per round
+    const int i0 = (it * kT + threadIdx.x) * 4;
+    int32_t x[4];
+    if (vec) {
+      const int4 q = __ldcs(reinterpret_cast<const int4*>(L + i0));
+      x[0] = q.x, x[1] = q.y, x[2] = q.z, x[3] = q.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) x[e] = i0 + e < valid ? __ldcs(L + i0 + e) : 1;
+    }
+    uint32_t packed = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      int k = 0;
+#pragma unroll
+      for (int q = 0; q < NB - 1; ++q) k += (x[e] > bnd[q]);  // == searchsorted(..., 'left')
+      anybad |= (uint32_t)(x[e] - 1) >= blast;               // len < 1 or len > last bound
+      packed |= (uint32_t)k << (e * CB);
+    }
+    const int nv = vec ? 4 : max(0, min(4, valid - i0));  // keys of this quad inside the tile
+    if (CB == 2) {  // counts of codes 1..3 from the 2-bit fields; code 0 = the rest
+      const uint32_t lo = packed & 0x55u, hi = (packed >> 1) & 0x55u;
+      c[1] += __popc(lo & ~hi);
+      if (NB > 2) c[2] += __popc(hi & ~lo);
+      if (NB > 3) c[3] += __popc(lo & hi);
+      c[0] += nv;  // minus the others at the end
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (e < nv) {
+          const int k = (int)((packed >> (e * CB)) & 15u);
+#pragma unroll
+          for (int q = 0; q < NB; ++q) c[q] += (k == q);
+        }
+    }
+    // lanes QPW*m .. QPW*m + QPW-1 hold one word's quads
+#pragma unroll
+    for (int o = 1; o < QPW; o <<= 1) packed |= __shfl_down_sync(0xffffffffu, packed, o) << (o * 4 * CB);
+    if ((lane & (QPW - 1)) == 0) cw[(i0 / 4) / QPW] = packed;
   }
-  int gt[NB];
-#pragma unroll
-  for (int q = 0; q < NB; ++q) gt[q] = 0;
-  int pos = 0, anybad = 0;
-#pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    const int32_t x = v[j];
-    pos += (x >= 1);
-#pragma unroll
-    for (int q = 0; q < NB; ++q) gt[q] += (x > bnd[q]);
-    anybad |= (x < 1) | (x > blast);
-  }
-  // padding slots were given length 1: they count in `pos` only; remove them
-  pos -= kItems - (valid > threadIdx.x ? (valid - 1 - (int)threadIdx.x) / kT + 1 : 0);
-  __syncthreads();  // cnt zeroed
-  if (__syncthreads_or(anybad)) {  // rare: locate the tile's first bad sample
+  if (CB == 2) c[0] -= c[1] + (NB > 2 ? c[2] : 0) + (NB > 3 ? c[3] : 0);
+  if (__syncthreads_or(anybad)) {  // rare: the tile's first bad sample (smallest index)
     long long first_bad = -1;
-#pragma unroll
-    for (int j = kItems - 1; j >= 0; --j) {  // keeps the smallest index
-      const int idx = j * kT + threadIdx.x;
-      if (idx < valid && (v[j] < 1 || v[j] > blast)) first_bad = lbase + idx;
+    for (int i = (int)threadIdx.x; i < valid && first_bad < 0; i += kT) {
+      const int32_t x = L[i];
+      if ((uint32_t)(x - 1) >= blast) first_bad = lbase + i;
     }
     if (first_bad >= 0) atomicMin(reinterpret_cast<unsigned long long*>(p.bad + g), (unsigned long long)first_bad);
   }
-  // stratum q < nb: gt[q-1] - gt[q] (q = 0: pos - gt[0]); warp sums, then one smem add per warp
 #pragma unroll
   for (int q = 0; q < NB; ++q) {
-    int c = (q == 0 ? pos : gt[q - 1]) - gt[q];
+    int v = c[q];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-    if ((threadIdx.x & 31) == 0 && c && q < p.nb) atomicAdd(&cnt[q], c);
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0 && v && q < p.nb) atomicAdd(&cnt[q], v);
   }
   __syncthreads();
   if (threadIdx.x < NB) p.tile_counts[(int64_t)tile * kMaxStrata + threadIdx.x] = threadIdx.x < p.nb ? cnt[threadIdx.x] : 0;
-
   // the shard's last tile to finish turns its tile counts into exclusive
   // prefixes (in place) and publishes the shard totals
   __shared__ bool s_last;
@@ -175,96 +190,124 @@ __global__ void __launch_bounds__(kT) k_strata_count(const __grid_constant__ Str
   if (threadIdx.x < p.nb) p.counts[(int64_t)g * p.nb + threadIdx.x] = s_tot[threadIdx.x];
 }
 
-// pass 2: each tile sums the counts of the earlier tiles of its shard (one L2
-// round trip, no separate scan launch), then scatters with stable in-tile
-// ranks from a single packed block scan, staged so runs are written coalesced
+// pass 2: scatter from the codes.  A warp owns 512 consecutive keys; the
+// tile's warps are offset by a shared-memory scan of their per-stratum
+// counts; inside a warp, 16 rounds of 32 keys in input order.  Lane k < nb
+// carries stratum k's next output slot (32-bit, within the shard).
+template <int NB, bool IDS, bool FULL>
+__device__ __forceinline__ void scatter_rounds(const StrataParams& p, const uint32_t (&word)[(kWarpKeys * code_bits<NB>() / 32) / 32],
+                                               int next, int32_t* out, const int32_t* ids, int wbase, int valid) {
+  constexpr int CB = code_bits<NB>();
+  constexpr int WPL = (kWarpKeys * CB / 32) / 32;  // code words per lane (1 or 2)
+  constexpr int KPW = 32 / CB;                     // keys per word
+  constexpr uint32_t CMASK = (1u << CB) - 1u;
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = (1u << lane) - 1u;
+  const int shift = (lane % KPW) * CB;  // field of this lane's key in its word (32 % KPW == 0)
+  uint32_t inv[CB];                     // lane k's code bits, as select masks
+#pragma unroll
+  for (int b = 0; b < CB; ++b) inv[b] = ((lane >> b) & 1) ? 0u : 0xffffffffu;
+#pragma unroll
+  for (int j = 0; j < kWarpKeys / 32; ++j) {
+    const int key = j * 32 + lane;   // warp-local key of this lane in round j
+    const int wi = key / KPW;        // its word (warp-local)
+    uint32_t wsel;
+    if constexpr (WPL == 1) {
+      wsel = __shfl_sync(0xffffffffu, word[0], wi);
+    } else {
+      const uint32_t a0 = __shfl_sync(0xffffffffu, word[0], wi >> 1), a1 = __shfl_sync(0xffffffffu, word[WPL - 1], wi >> 1);
+      wsel = (wi & 1) ? a1 : a0;
+    }
+    const bool ok = FULL || wbase + key < valid;
+    const int code = (int)((wsel >> shift) & CMASK);
+    const uint32_t live = FULL ? 0xffffffffu : __ballot_sync(0xffffffffu, ok);
+    uint32_t diff = 0, mk = live;  // lanes whose code differs from mine; lanes with code == lane
+#pragma unroll
+    for (int b = 0; b < CB; ++b) {
+      const uint32_t bits = __ballot_sync(0xffffffffu, (code >> b) & 1);
+      diff |= bits ^ (((code >> b) & 1) ? 0xffffffffu : 0u);
+      mk &= bits ^ inv[b];
+    }
+    const int base = __shfl_sync(0xffffffffu, next, code);
+    if (ok) out[base + __popc(~diff & live & lt)] = IDS ? __ldcs(ids + wbase + key) : wbase + key;
+    next += __popc(mk);
+  }
+}
+
 template <int NB>
 __global__ void __launch_bounds__(kT) k_strata_scatter(const __grid_constant__ StrataParams p) {
-  constexpr int NW = (NB + 3) / 4;
-  using Scan = cub::BlockScan<Packed<NW>, kT>;
-  __shared__ union {
-    typename LoadT::TempStorage ld;
-    typename Scan::TempStorage scan;
-    int32_t stage[kTile];
-  } sm;
-  __shared__ int32_t s_kof[kTile];       // stratum of each staged slot
-  __shared__ int64_t s_dst[kMaxStrata];  // global start of this tile's run, per stratum
-  __shared__ int32_t s_lstart[kMaxStrata + 1];
-  __shared__ unsigned long long s_pre[kMaxStrata], s_tot[kMaxStrata];
+  constexpr int CB = code_bits<NB>();
+  constexpr int WPT = kTile * CB / 32;           // code words per tile
+  constexpr int WPW = kWarpKeys * CB / 32;       // code words per warp (32 or 64)
+  constexpr int WPL = WPW / 32;                  // ... per lane (1 or 2)
+  constexpr int KPW = 32 / CB;                   // keys per word
+  __shared__ int s_wcnt[kT / 32][kMaxStrata];
+  __shared__ int s_dst[kMaxStrata];
   const int tile = blockIdx.x;
   const int g = shard_of_tile(p, tile);
   const int64_t sbeg = p.shard_off[g], send = p.shard_off[g + 1];
   const int64_t lbase = (int64_t)(tile - p.tile_off[g]) * kTile;
   const int valid = (int)min64(kTile, send - sbeg - lbase);
-  if (threadIdx.x < kMaxStrata) {  // this tile's exclusive prefix + the shard totals (from pass 1)
-    const bool in = threadIdx.x < p.nb;
-    s_pre[threadIdx.x] = in ? (unsigned long long)p.tile_counts[(int64_t)tile * kMaxStrata + threadIdx.x] : 0ull;
-    s_tot[threadIdx.x] = in ? (unsigned long long)p.counts[(int64_t)g * p.nb + threadIdx.x] : 0ull;
-  }
-  int32_t v[kItems];
-  LoadT(sm.ld).Load(p.len + sbeg + lbase, v, valid, 1);
-  __syncthreads();
-  int32_t id[kItems];
-  if (p.ids) {
-    LoadT(sm.ld).Load(p.ids + sbeg + lbase, id, valid, 0);
-    __syncthreads();
-  } else {
-#pragma unroll
-    for (int j = 0; j < kItems; ++j) id[j] = (int32_t)(lbase + threadIdx.x * kItems + j);
-  }
-  int8_t kk[kItems];
-  Packed<NW> mine;
-#pragma unroll
-  for (int i = 0; i < NW; ++i) mine.w[i] = 0;
-#pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    const int idx = threadIdx.x * kItems + j;
-    int k = -1;
-    if (idx < valid) {
-      k = stratum_of<NB>(v[j], p);
-      if (k >= p.nb || v[j] < 1) k = -1;  // bad samples are reported, not placed
-    }
-    kk[j] = (int8_t)k;
-    if (k >= 0) mine.w[k >> 2] += 1ull << ((k & 3) * 16);
-  }
-  Packed<NW> ex, agg;
-  Scan(sm.scan).ExclusiveSum(mine, ex, agg);
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    int64_t gbase = sbeg;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {  // this tile's first slot per stratum (in-shard): earlier strata + earlier tiles
+    int gb = 0;
     for (int k = 0; k < p.nb; ++k) {
-      s_lstart[k] = acc;
-      acc += (int)agg.field(k);
-      s_dst[k] = gbase + (int64_t)s_pre[k];
-      gbase += (int64_t)s_tot[k];
+      s_dst[k] = gb + p.tile_counts[(int64_t)tile * kMaxStrata + k];
+      gb += (int)p.counts[(int64_t)g * p.nb + k];
     }
-    s_lstart[p.nb] = acc;
   }
-  __syncthreads();  // also retires the scan temp storage before staging
-  unsigned run[NB];
+  const int wbeg = w * kWarpKeys;  // first key of this warp in the tile
+  uint32_t word[WPL];
+  const uint32_t* cw = p.codes + (int64_t)tile * WPT + w * WPW;
 #pragma unroll
-  for (int k = 0; k < NB; ++k) run[k] = 0;
+  for (int i = 0; i < WPL; ++i) word[i] = __ldcs(cw + lane * WPL + i);
+  // per-stratum counts of this warp's keys (keys beyond `valid` masked out)
+  int mine[NB];
 #pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    const int k = kk[j];
-    if (k >= 0) {
-      unsigned r = 0;
+  for (int k = 0; k < NB; ++k) mine[k] = 0;
 #pragma unroll
-      for (int q = 0; q < NB; ++q)
-        if (q == k) {
-          r = run[q];
-          run[q] = r + 1;
-        }
-      const int slot = s_lstart[k] + (int)ex.field(k) + (int)r;
-      sm.stage[slot] = id[j];
-      s_kof[slot] = k;
+  for (int i = 0; i < WPL; ++i) {
+    const int k0 = wbeg + (lane * WPL + i) * KPW;  // first key of this word
+    const int nv = max(0, min(KPW, valid - k0));
+    const uint32_t vmask = nv >= KPW ? 0xffffffffu : ((1u << (nv * CB)) - 1u);
+    uint32_t low = 0;
+#pragma unroll
+    for (int f = 0; f < KPW; ++f) low |= 1u << (f * CB);
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      // fields equal to k: XOR with k replicated, then fields that are all-zero
+      const uint32_t y = word[i] ^ (low * (uint32_t)k);
+      uint32_t z = y;
+#pragma unroll
+      for (int b = 1; b < CB; ++b) z |= y >> b;  // low bit of each field = OR of the field's bits
+      mine[k] += __popc(~z & low & vmask);
     }
+  }
+#pragma unroll
+  for (int k = 0; k < NB; ++k) {
+    int v = mine[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == k) s_wcnt[w][k] = v;
   }
   __syncthreads();
-  const int placed = s_lstart[p.nb];
-  for (int slot = threadIdx.x; slot < placed; slot += kT) {
-    const int k = s_kof[slot];
-    p.ids_out[s_dst[k] + (slot - s_lstart[k])] = sm.stage[slot];
+  int next = 0;  // lane k < nb: next output slot of stratum k for this warp (within the shard)
+  if (lane < p.nb) {
+    int off = s_dst[lane];
+    for (int u = 0; u < w; ++u) off += s_wcnt[u][lane];
+    next = off;
+  }
+  int32_t* out = p.ids_out + sbeg;
+  const int wbase = (int)lbase + wbeg;  // shard-local index of this warp's first key
+  const int32_t* ids = p.ids ? p.ids + sbeg : nullptr;
+  const int wvalid = (int)lbase + valid;
+  const bool full = wbeg + kWarpKeys <= valid;
+  if (full) {
+    if (ids) scatter_rounds<NB, true, true>(p, word, next, out, ids, wbase, wvalid);
+    else scatter_rounds<NB, false, true>(p, word, next, out, ids, wbase, wvalid);
+  } else {
+    if (ids) scatter_rounds<NB, true, false>(p, word, next, out, ids, wbase, wvalid);
+    else scatter_rounds<NB, false, false>(p, word, next, out, ids, wbase, wvalid);
   }
 }
 
@@ -275,10 +318,14 @@ using namespace b2;
 
 static inline int64_t strata_tiles(int64_t n) { return (n + kTile - 1) / kTile; }
 
+static inline size_t strata_ws_bytes(int64_t tiles) {
+  // per-shard tile tickets; per-tile counts; per-tile codes (4 bits/key: room for 16 strata)
+  return kMaxShards * sizeof(unsigned) + (size_t)tiles * kMaxStrata * sizeof(int32_t) + (size_t)tiles * (kTile / 2);
+}
+
 extern "C" size_t b2_strata_workspace_bytes(int64_t n) {
   if (n < 1) n = 1;
-  // per-shard tile tickets; per-tile counts (+ one partial tile per shard boundary)
-  return kMaxShards * sizeof(unsigned) + (size_t)(strata_tiles(n) + kMaxShards) * kMaxStrata * sizeof(int32_t);
+  return strata_ws_bytes(strata_tiles(n) + kMaxShards);  // + one partial tile per shard boundary
 }
 
 extern "C" int b2_strata_partition_shards(const int32_t* lengths, const int32_t* ids, const int64_t* shard_off,
@@ -307,10 +354,11 @@ extern "C" int b2_strata_partition_shards(const int32_t* lengths, const int32_t*
     T += strata_tiles(n);
   }
   p.tile_off[nshard] = (int32_t)T;
-  const size_t need = kMaxShards * sizeof(unsigned) + (size_t)T * kMaxStrata * sizeof(int32_t);
+  const size_t need = strata_ws_bytes(T);
   B2_REQUIRE(workspace && workspace_bytes >= need, B2_ERR_INVALID, "strata workspace needs %zu bytes", need);
   p.shard_done = static_cast<unsigned*>(workspace);
   p.tile_counts = reinterpret_cast<int32_t*>(static_cast<char*>(workspace) + kMaxShards * sizeof(unsigned));
+  p.codes = reinterpret_cast<uint32_t*>(p.tile_counts + T * kMaxStrata);
   p.counts = counts;
   p.bad = bad;
   p.ids_out = ids_out;

@@ -78,7 +78,8 @@ def test_stratify_kats():
 
 
 @pytest.mark.parametrize("n", [1, 4095, 4096, 4097, 100_003])
-@pytest.mark.parametrize("bounds", [BOUNDS, (512,), (10, 20, 30, 40, 50, 60, 70, 80, 90, 100, 200, 300, 400, 450, 500, 512)])
+@pytest.mark.parametrize("bounds", [BOUNDS, (512,), (100, 300, 512), (50, 100, 150, 200, 300, 400, 512),
+                                    (10, 20, 30, 40, 50, 60, 70, 80, 90, 100, 200, 300, 400, 450, 500, 512)])
 def test_stratify_sizes_vs_oracle(n, bounds):
     rng = np.random.default_rng(n + len(bounds))
     lens = rng.integers(1, 513, size=n).astype(np.int32)
