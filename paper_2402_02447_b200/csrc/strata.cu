@@ -96,17 +96,23 @@ __global__ void __launch_bounds__(kT) k_strata_count(const __grid_constant__ Str
   for (int q = 0; q < NB; ++q) c[q] = 0;
   bool anybad = false;
   uint32_t* cw = p.codes + (int64_t)tile * WPT;
+  constexpr int R = kTile / (4 * kT);  // rounds of 4 consecutive keys per thread
+  int32_t xs[R][4];
 #pragma unroll
-  for (int it = 0; it < kTile / (4 * kT); ++it) {  // 4 consecutive keys per thread per round
+  for (int it = 0; it < R; ++it) {  // every load issued before any use
     const int i0 = (it * kT + threadIdx.x) * 4;
-    int32_t x[4];
     if (vec) {
       const int4 q = __ldcs(reinterpret_cast<const int4*>(L + i0));
-      x[0] = q.x, x[1] = q.y, x[2] = q.z, x[3] = q.w;
+      xs[it][0] = q.x, xs[it][1] = q.y, xs[it][2] = q.z, xs[it][3] = q.w;
     } else {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) x[e] = i0 + e < valid ? __ldcs(L + i0 + e) : 1;
+      for (int e = 0; e < 4; ++e) xs[it][e] = i0 + e < valid ? __ldcs(L + i0 + e) : 1;
     }
+  }
+#pragma unroll
+  for (int it = 0; it < R; ++it) {
+    const int i0 = (it * kT + threadIdx.x) * 4;
+    const int32_t* x = xs[it];
     uint32_t packed = 0;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -154,11 +160,13 @@ __global__ void __launch_bounds__(kT) k_strata_count(const __grid_constant__ Str
     if (lane == 0 && v && q < p.nb) atomicAdd(&cnt[q], v);
   }
   __syncthreads();
-  if (threadIdx.x < NB) p.tile_counts[(int64_t)tile * kMaxStrata + threadIdx.x] = threadIdx.x < p.nb ? cnt[threadIdx.x] : 0;
+  if (threadIdx.x < NB) {
+    p.tile_counts[(int64_t)tile * kMaxStrata + threadIdx.x] = threadIdx.x < p.nb ? cnt[threadIdx.x] : 0;
+    __threadfence();  // the counts are visible before this tile's ticket
+  }
   // the shard's last tile to finish turns its tile counts into exclusive
   // prefixes (in place) and publishes the shard totals
   __shared__ bool s_last;
-  __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
     const unsigned nt = (unsigned)(p.tile_off[g + 1] - p.tile_off[g]);
@@ -234,6 +242,34 @@ __device__ __forceinline__ void scatter_rounds(const StrataParams& p, const uint
   }
 }
 
+// NB <= 4 (2-bit codes, one word of 16 keys per lane): the lane holding word
+// wi precomputes, for each code c, the slot of the first key of code c in
+// that word (stratum base + count of code c in earlier words of the warp);
+// a key's slot is that value for its own code (four shuffles from the
+// holder, a select) + the count of its code in the earlier fields of the
+// word.  No per-round ballots, scans or base updates.
+template <bool IDS, bool FULL>
+__device__ __forceinline__ void scatter_rounds_prefix(uint32_t word, const int (&slot)[4], int32_t* out,
+                                                      const int32_t* ids, int wbase, int valid) {
+  constexpr uint32_t LOW = 0x55555555u;
+  const int lane = threadIdx.x & 31;
+  const int f = lane & 15, half = lane >> 4;
+  const uint32_t below = LOW & ((1u << (2 * f)) - 1u);  // low bits of the fields before this lane's field
+#pragma unroll
+  for (int j = 0; j < kWarpKeys / 32; ++j) {
+    const int wi = 2 * j + half;  // word of this lane's key in round j
+    const int key = j * 32 + lane;
+    const uint32_t wv = __shfl_sync(0xffffffffu, word, wi);
+    const int s0 = __shfl_sync(0xffffffffu, slot[0], wi), s1 = __shfl_sync(0xffffffffu, slot[1], wi);
+    const int s2 = __shfl_sync(0xffffffffu, slot[2], wi), s3 = __shfl_sync(0xffffffffu, slot[3], wi);
+    const uint32_t code = (wv >> (2 * f)) & 3u;
+    const uint32_t y = wv ^ (LOW * code);
+    const int inword = __popc(~(y | (y >> 1)) & below);
+    const int sc = (code & 2u) ? ((code & 1u) ? s3 : s2) : ((code & 1u) ? s1 : s0);
+    if (FULL || wbase + key < valid) out[sc + inword] = IDS ? __ldcs(ids + wbase + key) : wbase + key;
+  }
+}
+
 template <int NB>
 __global__ void __launch_bounds__(kT) k_strata_scatter(const __grid_constant__ StrataParams p) {
   constexpr int CB = code_bits<NB>();
@@ -261,7 +297,58 @@ __global__ void __launch_bounds__(kT) k_strata_scatter(const __grid_constant__ S
   const uint32_t* cw = p.codes + (int64_t)tile * WPT + w * WPW;
 #pragma unroll
   for (int i = 0; i < WPL; ++i) word[i] = __ldcs(cw + lane * WPL + i);
-  // per-stratum counts of this warp's keys (keys beyond `valid` masked out)
+  if constexpr (CB == 2) {
+    // per-word counts of codes 0..2 (keys beyond `valid` masked out), packed 10 bits each
+    constexpr uint32_t LOW = 0x55555555u;
+    const int k0 = wbeg + lane * 16;
+    const int nv = max(0, min(16, valid - k0));
+    const uint32_t vmask = nv >= 16 ? 0xffffffffu : ((1u << (nv * 2)) - 1u);
+    uint32_t pk = 0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const uint32_t y = word[0] ^ (LOW * (uint32_t)k);
+      pk |= (uint32_t)__popc(~(y | (y >> 1)) & LOW & vmask) << (10 * k);
+    }
+    uint32_t inc = pk;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+    const int wkeys = max(0, min(kWarpKeys, valid - wbeg));
+    if (lane < 4) {
+      const int t0 = (int)(tot & 1023u), t1 = (int)((tot >> 10) & 1023u), t2 = (int)(tot >> 20);
+      s_wcnt[w][lane] = lane == 0 ? t0 : lane == 1 ? t1 : lane == 2 ? t2 : wkeys - t0 - t1 - t2;
+    }
+    __syncthreads();
+    int next = 0;  // lane k < nb: first slot of stratum k for this warp (within the shard)
+    if (lane < p.nb) {
+      int off = s_dst[lane];
+      for (int u = 0; u < w; ++u) off += s_wcnt[u][lane];
+      next = off;
+    }
+    int32_t* out = p.ids_out + sbeg;
+    const int wbase = (int)lbase + wbeg;  // shard-local index of this warp's first key
+    const int32_t* ids = p.ids ? p.ids + sbeg : nullptr;
+    const int wvalid = (int)lbase + valid;
+    const uint32_t ex = inc - pk;  // codes 0..2 in the warp's earlier words
+    const int e0 = (int)(ex & 1023u), e1 = (int)((ex >> 10) & 1023u), e2 = (int)(ex >> 20);
+    int slot[4];
+    slot[0] = __shfl_sync(0xffffffffu, next, 0) + e0;
+    slot[1] = __shfl_sync(0xffffffffu, next, 1) + e1;
+    slot[2] = __shfl_sync(0xffffffffu, next, 2) + e2;
+    slot[3] = __shfl_sync(0xffffffffu, next, 3) + 16 * lane - e0 - e1 - e2;  // earlier words are full
+    if (wbeg + kWarpKeys <= valid) {
+      if (ids) scatter_rounds_prefix<true, true>(word[0], slot, out, ids, wbase, wvalid);
+      else scatter_rounds_prefix<false, true>(word[0], slot, out, ids, wbase, wvalid);
+    } else {
+      if (ids) scatter_rounds_prefix<true, false>(word[0], slot, out, ids, wbase, wvalid);
+      else scatter_rounds_prefix<false, false>(word[0], slot, out, ids, wbase, wvalid);
+    }
+    return;
+  } else {
+    // per-stratum counts of this warp's keys (keys beyond `valid` masked out)
   int mine[NB];
 #pragma unroll
   for (int k = 0; k < NB; ++k) mine[k] = 0;
@@ -309,6 +396,7 @@ __global__ void __launch_bounds__(kT) k_strata_scatter(const __grid_constant__ S
     if (ids) scatter_rounds<NB, true, false>(p, word, next, out, ids, wbase, wvalid);
     else scatter_rounds<NB, false, false>(p, word, next, out, ids, wbase, wvalid);
   }
+  }
 }
 
 }  // namespace
@@ -317,6 +405,7 @@ __global__ void __launch_bounds__(kT) k_strata_scatter(const __grid_constant__ S
 using namespace b2;
 
 static inline int64_t strata_tiles(int64_t n) { return (n + kTile - 1) / kTile; }
+
 
 static inline size_t strata_ws_bytes(int64_t tiles) {
   // per-shard tile tickets; per-tile counts; per-tile codes (4 bits/key: room for 16 strata)
