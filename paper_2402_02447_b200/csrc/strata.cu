@@ -4,23 +4,26 @@
 // searchsorted(bounds, length, side='left') (:74), samples are appended to
 // their stratum in input order (:81), probs = count/N (:82; host side).
 //
-// Two launches for ALL rank shards at once.  Algorithmic traffic is 8 B/key
+// Three launches for ALL rank shards at once.  Algorithmic traffic is 8 B/key
 // (4 B length read, 4 B id written; +4 B if explicit ids are read); the
 // launches move 8.5 B/key (2-bit stratum codes, 4-bit above 4 strata):
 //   k_strata_count  : one CTA per 4096-key tile reads the lengths once (16 B
-//                     vector loads), writes each key's stratum CODE packed 16
-//                     per word (0.25 B/key), counts per tile and stratum, and,
-//                     in the LAST tile of each shard to finish (atomic
-//                     ticket), turns the shard's tile counts into exclusive
-//                     prefixes (in place) and writes the shard totals;
+//                     vector loads, all issued up front), writes each key's
+//                     stratum CODE packed 16 per word (0.25 B/key) and the
+//                     tile's per-stratum counts — no tail, so CTAs retire as
+//                     soon as their stores are issued;
+//   k_strata_scan   : one CTA per shard turns the tile counts into exclusive
+//                     in-shard prefixes and writes the shard totals;
 //   k_strata_scatter: one CTA per tile, one warp per 512 keys, reads only the
-//                     codes: warp counts from the packed words, the tile's
-//                     warps scanned in shared memory, then 16 rounds of 32 keys
-//                     in input order — a key's rank among the round's keys of
-//                     its stratum comes from CB ballots (one per code bit), its
-//                     run base from the lane that owns that stratum (shuffle)
-//                     — and each id is stored straight to its final slot (a
-//                     round writes <= nb contiguous runs: coalesced, no staging).
+//                     codes.  A warp counts its words with bit tricks, the
+//                     tile's warps are offset through shared memory; with <= 4
+//                     strata each lane then holds, for its word, the first
+//                     output slot of every code, and a key's slot is that
+//                     slot (four shuffles + a select) + the count of its code
+//                     in the earlier fields of its word; with more strata a
+//                     round's ranks come from one ballot per code bit.  Each
+//                     id is stored straight to its final slot (a round writes
+//                     <= nb contiguous runs: coalesced, no staging).
 // A bad sample (length < 1 or above the last bound) is reported through
 // `bad` (the wrapper raises like the reference); it is placed in the nearest
 // stratum, so ids_out/counts of that shard are unspecified.
@@ -38,6 +41,7 @@ constexpr int kT = 256;            // threads per tile CTA
 constexpr int kTile = 4096;        // keys per tile (8 warps x 512)
 constexpr int kWarpKeys = 512;     // keys per warp in the scatter
 constexpr int kMaxShards = 64;     // shards (segments) per launch
+constexpr int kScanT = 1024;       // threads of the per-shard tile-count scan
 
 struct StrataParams {
   const int32_t* len;
@@ -47,7 +51,6 @@ struct StrataParams {
   int64_t shard_off[kMaxShards + 1];  // element offset of each shard
   int32_t tile_off[kMaxShards + 1];   // first tile of each shard
   int32_t* tile_counts;               // [T][kMaxStrata]: counts, then exclusive in-shard prefixes
-  unsigned* shard_done;               // [kMaxShards] tiles counted per shard (zeroed per launch)
   uint32_t* codes;                    // [T][kTile * CB / 32] packed stratum codes
   int64_t* counts;                    // [nshard][nb] totals
   int64_t* bad;                       // [nshard] first bad index within the shard (u64 min), pre-set to -1
@@ -67,8 +70,7 @@ __device__ __forceinline__ int shard_of_tile(const StrataParams& p, int tile) {
   return lo;
 }
 
-// pass 1: codes + per-tile counts (+ the shard's first bad sample), then the
-// shard's last tile scans the tile counts into prefixes.  The code is
+// pass 1: codes + per-tile counts (+ the shard's first bad sample).  The code is
 // sum_{q < nb-1} (len > bound_q): a length above the last bound lands in the
 // last stratum and one below 1 in the first, so bad samples need no branch.
 template <int NB>
@@ -160,42 +162,49 @@ __global__ void __launch_bounds__(kT) k_strata_count(const __grid_constant__ Str
     if (lane == 0 && v && q < p.nb) atomicAdd(&cnt[q], v);
   }
   __syncthreads();
-  if (threadIdx.x < NB) {
-    p.tile_counts[(int64_t)tile * kMaxStrata + threadIdx.x] = threadIdx.x < p.nb ? cnt[threadIdx.x] : 0;
-    __threadfence();  // the counts are visible before this tile's ticket
-  }
-  // the shard's last tile to finish turns its tile counts into exclusive
-  // prefixes (in place) and publishes the shard totals
-  __shared__ bool s_last;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned nt = (unsigned)(p.tile_off[g + 1] - p.tile_off[g]);
-    s_last = atomicAdd(&p.shard_done[g], 1u) == nt - 1;
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  const int t0 = p.tile_off[g], t1 = p.tile_off[g + 1], nt = t1 - t0;
-  const int per = (nt + kT - 1) / kT;  // contiguous tiles per thread
-  const int a = min(t0 + (int)threadIdx.x * per, t1), b = min(a + per, t1);
-  using Scan = cub::BlockScan<int, kT>;
+  if (threadIdx.x < NB) p.tile_counts[(int64_t)tile * kMaxStrata + threadIdx.x] = threadIdx.x < p.nb ? cnt[threadIdx.x] : 0;
+}
+
+// pass 1b: one CTA per shard turns its tile counts into exclusive in-shard
+// prefixes (in place) and writes the shard totals.  Each thread owns a run
+// of consecutive tiles and reads each tile's count row once (16 B vectors);
+// the NB block scans run back to back on register sums.
+template <int NB>
+__global__ void __launch_bounds__(kScanT) k_strata_scan(const __grid_constant__ StrataParams p) {
+  using Scan = cub::BlockScan<int, kScanT>;
   __shared__ typename Scan::TempStorage scan;
-  __shared__ int64_t s_tot[NB];
-  for (int k = 0; k < NB; ++k) {
-    int sum = 0;
-    for (int t = a; t < b; ++t) sum += __ldcg(&p.tile_counts[(int64_t)t * kMaxStrata + k]);
-    int ex, agg;
-    Scan(scan).ExclusiveSum(sum, ex, agg);
-    for (int t = a; t < b; ++t) {
-      int32_t* c = &p.tile_counts[(int64_t)t * kMaxStrata + k];
-      const int v = __ldcg(c);
-      *c = ex;
-      ex += v;
+  const int g = blockIdx.x;
+  const int t0 = p.tile_off[g], t1 = p.tile_off[g + 1], nt = t1 - t0;
+  const int per = (nt + kScanT - 1) / kScanT;  // contiguous tiles per thread
+  const int a = min(t0 + (int)threadIdx.x * per, t1), b = min(a + per, t1);
+  int sum[NB];
+#pragma unroll
+  for (int k = 0; k < NB; ++k) sum[k] = 0;
+  for (int t = a; t < b; ++t) {
+    const int4* row = reinterpret_cast<const int4*>(p.tile_counts + (int64_t)t * kMaxStrata);
+#pragma unroll
+    for (int q = 0; q < NB / 4; ++q) {
+      const int4 v = row[q];
+      sum[4 * q] += v.x, sum[4 * q + 1] += v.y, sum[4 * q + 2] += v.z, sum[4 * q + 3] += v.w;
     }
-    if (threadIdx.x == 0) s_tot[k] = agg;
-    __syncthreads();  // scan storage reuse
   }
-  if (threadIdx.x < p.nb) p.counts[(int64_t)g * p.nb + threadIdx.x] = s_tot[threadIdx.x];
+  int ex[NB];
+#pragma unroll
+  for (int k = 0; k < NB; ++k) {
+    int agg;
+    if (k) __syncthreads();  // scan storage reuse
+    Scan(scan).ExclusiveSum(sum[k], ex[k], agg);
+    if (threadIdx.x == 0 && k < p.nb) p.counts[(int64_t)g * p.nb + k] = agg;
+  }
+  for (int t = a; t < b; ++t) {
+    int4* row = reinterpret_cast<int4*>(p.tile_counts + (int64_t)t * kMaxStrata);
+#pragma unroll
+    for (int q = 0; q < NB / 4; ++q) {
+      const int4 v = row[q];
+      row[q] = make_int4(ex[4 * q], ex[4 * q + 1], ex[4 * q + 2], ex[4 * q + 3]);
+      ex[4 * q] += v.x, ex[4 * q + 1] += v.y, ex[4 * q + 2] += v.z, ex[4 * q + 3] += v.w;
+    }
+  }
 }
 
 // pass 2: scatter from the codes.  A warp owns 512 consecutive keys; the
@@ -243,13 +252,13 @@ __device__ __forceinline__ void scatter_rounds(const StrataParams& p, const uint
 }
 
 // NB <= 4 (2-bit codes, one word of 16 keys per lane): the lane holding word
-// wi precomputes, for each code c, the slot of the first key of code c in
-// that word (stratum base + count of code c in earlier words of the warp);
-// a key's slot is that value for its own code (four shuffles from the
-// holder, a select) + the count of its code in the earlier fields of the
-// word.  No per-round ballots, scans or base updates.
+// wi writes, for each code c, the slot of the first key of code c in that
+// word (stratum base + count of code c in earlier words of the warp) to a
+// shared [word][code] table; a key's slot is its (word, code) entry + the
+// count of its code in the earlier fields of the word.  No per-round
+// ballots, scans or base updates.
 template <bool IDS, bool FULL>
-__device__ __forceinline__ void scatter_rounds_prefix(uint32_t word, const int (&slot)[4], int32_t* out,
+__device__ __forceinline__ void scatter_rounds_prefix(uint32_t word, const int* slot_tab, int32_t* out,
                                                       const int32_t* ids, int wbase, int valid) {
   constexpr uint32_t LOW = 0x55555555u;
   const int lane = threadIdx.x & 31;
@@ -260,12 +269,10 @@ __device__ __forceinline__ void scatter_rounds_prefix(uint32_t word, const int (
     const int wi = 2 * j + half;  // word of this lane's key in round j
     const int key = j * 32 + lane;
     const uint32_t wv = __shfl_sync(0xffffffffu, word, wi);
-    const int s0 = __shfl_sync(0xffffffffu, slot[0], wi), s1 = __shfl_sync(0xffffffffu, slot[1], wi);
-    const int s2 = __shfl_sync(0xffffffffu, slot[2], wi), s3 = __shfl_sync(0xffffffffu, slot[3], wi);
     const uint32_t code = (wv >> (2 * f)) & 3u;
     const uint32_t y = wv ^ (LOW * code);
     const int inword = __popc(~(y | (y >> 1)) & below);
-    const int sc = (code & 2u) ? ((code & 1u) ? s3 : s2) : ((code & 1u) ? s1 : s0);
+    const int sc = slot_tab[wi * 4 + (int)code];
     if (FULL || wbase + key < valid) out[sc + inword] = IDS ? __ldcs(ids + wbase + key) : wbase + key;
   }
 }
@@ -279,6 +286,7 @@ __global__ void __launch_bounds__(kT) k_strata_scatter(const __grid_constant__ S
   constexpr int KPW = 32 / CB;                   // keys per word
   __shared__ int s_wcnt[kT / 32][kMaxStrata];
   __shared__ int s_dst[kMaxStrata];
+  __shared__ __align__(16) int s_slot[kT / 32][CB == 2 ? 32 * 4 : 1];  // [word][code] first slots (<= 4 strata)
   const int tile = blockIdx.x;
   const int g = shard_of_tile(p, tile);
   const int64_t sbeg = p.shard_off[g], send = p.shard_off[g + 1];
@@ -334,17 +342,19 @@ __global__ void __launch_bounds__(kT) k_strata_scatter(const __grid_constant__ S
     const int wvalid = (int)lbase + valid;
     const uint32_t ex = inc - pk;  // codes 0..2 in the warp's earlier words
     const int e0 = (int)(ex & 1023u), e1 = (int)((ex >> 10) & 1023u), e2 = (int)(ex >> 20);
-    int slot[4];
-    slot[0] = __shfl_sync(0xffffffffu, next, 0) + e0;
-    slot[1] = __shfl_sync(0xffffffffu, next, 1) + e1;
-    slot[2] = __shfl_sync(0xffffffffu, next, 2) + e2;
-    slot[3] = __shfl_sync(0xffffffffu, next, 3) + 16 * lane - e0 - e1 - e2;  // earlier words are full
+    // this word's first slot per code (stratum base + the code's keys in earlier words)
+    int* tab = s_slot[w];
+    reinterpret_cast<int4*>(tab)[lane] = make_int4(
+        __shfl_sync(0xffffffffu, next, 0) + e0, __shfl_sync(0xffffffffu, next, 1) + e1,
+        __shfl_sync(0xffffffffu, next, 2) + e2,
+        __shfl_sync(0xffffffffu, next, 3) + 16 * lane - e0 - e1 - e2);  // earlier words are full
+    __syncwarp();
     if (wbeg + kWarpKeys <= valid) {
-      if (ids) scatter_rounds_prefix<true, true>(word[0], slot, out, ids, wbase, wvalid);
-      else scatter_rounds_prefix<false, true>(word[0], slot, out, ids, wbase, wvalid);
+      if (ids) scatter_rounds_prefix<true, true>(word[0], tab, out, ids, wbase, wvalid);
+      else scatter_rounds_prefix<false, true>(word[0], tab, out, ids, wbase, wvalid);
     } else {
-      if (ids) scatter_rounds_prefix<true, false>(word[0], slot, out, ids, wbase, wvalid);
-      else scatter_rounds_prefix<false, false>(word[0], slot, out, ids, wbase, wvalid);
+      if (ids) scatter_rounds_prefix<true, false>(word[0], tab, out, ids, wbase, wvalid);
+      else scatter_rounds_prefix<false, false>(word[0], tab, out, ids, wbase, wvalid);
     }
     return;
   } else {
@@ -406,10 +416,17 @@ using namespace b2;
 
 static inline int64_t strata_tiles(int64_t n) { return (n + kTile - 1) / kTile; }
 
+template <int NB>
+static cudaError_t launch_all(const StrataParams& p, int64_t T, cudaStream_t st) {
+  k_strata_count<NB><<<(unsigned)T, kT, 0, st>>>(p);
+  k_strata_scan<NB><<<(unsigned)p.nshard, kScanT, 0, st>>>(p);
+  k_strata_scatter<NB><<<(unsigned)T, kT, 0, st>>>(p);
+  return cudaGetLastError();
+}
 
 static inline size_t strata_ws_bytes(int64_t tiles) {
-  // per-shard tile tickets; per-tile counts; per-tile codes (4 bits/key: room for 16 strata)
-  return kMaxShards * sizeof(unsigned) + (size_t)tiles * kMaxStrata * sizeof(int32_t) + (size_t)tiles * (kTile / 2);
+  // per-tile counts; per-tile codes (4 bits/key: room for 16 strata)
+  return (size_t)tiles * kMaxStrata * sizeof(int32_t) + (size_t)tiles * (kTile / 2);
 }
 
 extern "C" size_t b2_strata_workspace_bytes(int64_t n) {
@@ -445,28 +462,16 @@ extern "C" int b2_strata_partition_shards(const int32_t* lengths, const int32_t*
   p.tile_off[nshard] = (int32_t)T;
   const size_t need = strata_ws_bytes(T);
   B2_REQUIRE(workspace && workspace_bytes >= need, B2_ERR_INVALID, "strata workspace needs %zu bytes", need);
-  p.shard_done = static_cast<unsigned*>(workspace);
-  p.tile_counts = reinterpret_cast<int32_t*>(static_cast<char*>(workspace) + kMaxShards * sizeof(unsigned));
+  p.tile_counts = static_cast<int32_t*>(workspace);
   p.codes = reinterpret_cast<uint32_t*>(p.tile_counts + T * kMaxStrata);
   p.counts = counts;
   p.bad = bad;
   p.ids_out = ids_out;
   cudaStream_t st = (cudaStream_t)stream;
   B2_CHECK(cudaMemsetAsync(bad, 0xff, sizeof(int64_t) * nshard, st));
-  B2_CHECK(cudaMemsetAsync(p.shard_done, 0, sizeof(unsigned) * nshard, st));
-  if (nb <= 4) {
-    k_strata_count<4><<<(unsigned)T, kT, 0, st>>>(p);
-    B2_CHECK(cudaGetLastError());
-    k_strata_scatter<4><<<(unsigned)T, kT, 0, st>>>(p);
-  } else if (nb <= 8) {
-    k_strata_count<8><<<(unsigned)T, kT, 0, st>>>(p);
-    B2_CHECK(cudaGetLastError());
-    k_strata_scatter<8><<<(unsigned)T, kT, 0, st>>>(p);
-  } else {
-    k_strata_count<16><<<(unsigned)T, kT, 0, st>>>(p);
-    B2_CHECK(cudaGetLastError());
-    k_strata_scatter<16><<<(unsigned)T, kT, 0, st>>>(p);
-  }
+  if (nb <= 4) B2_CHECK(launch_all<4>(p, T, st));
+  else if (nb <= 8) B2_CHECK(launch_all<8>(p, T, st));
+  else B2_CHECK(launch_all<16>(p, T, st));
   B2_CHECK(cudaGetLastError());
   return B2_OK;
 }
