@@ -380,8 +380,29 @@ def bench_clip(args, rank, world, local):
     e2e_s = max_over_ranks(time.perf_counter() - ts, world) / e2e_steps
     res["e2e"] = {"value": world * dim * 4 / e2e_s / 1e9, "unit": "GB/s", "ms_per_step": e2e_s * 1e3,
                   "h2d_bytes_per_step": dim * 4, "d2h_bytes_per_step": d2h, "steps": e2e_steps, "api": api}
-    res["_cpu_sample"] = g[: layout[0][1]].cpu().numpy()  # first bucket for the CPU baseline
     del host
+    if world == 1:
+        # the drop-in call exactly as a reference user makes it: a host fp64 (1, D) numpy array
+        # through GradientState + sync_bucketwise, host fp64 result (pageable copies both ways)
+        w64 = g.double().cpu().numpy()[None, :]
+        st_ = B.GradientState(w64, layout)
+        B.sync_bucketwise(st_, cfg)
+        del st_
+        torch.cuda.synchronize()
+        times = []
+        for _ in range(2):
+            t = time.perf_counter()
+            out64 = B.sync_bucketwise(B.GradientState(w64, layout), cfg)
+            times.append(time.perf_counter() - t)
+        dt = min(times)
+        res["e2e_drop_in"] = {
+            "value": dim * 4 / dt / 1e9, "unit": "GB/s", "ms_per_step": dt * 1e3,
+            "h2d_bytes_per_step": dim * 8, "d2h_bytes_per_step": dim * 8, "steps": len(times),
+            "api": "sync_bucketwise(GradientState(numpy float64 (1, D), layout), ClipConfig(1.0, 'bucket_wise')) "
+                   "-> numpy float64: the reference's own call (fp64 H2D from the caller's pageable array, "
+                   "fp64 result D2H into pinned memory)",
+            "result_type": type(out64).__name__}
+        del w64, out64
     return res
 
 
@@ -565,7 +586,101 @@ def bench_presort(args):
         "k3_presort_deal": {"ms": t3, "achieved_gbs": b_ids.numel() * 12 / (t3 * 1e-3) / 1e9,
                             "frac": b_ids.numel() * 12 / (t3 * 1e-3) / 1e9 / hbm},
         "note": "corpus and epoch pools tiled 10x (inputs 0.4-1.2 GB >> L2)"}
+    del big_lens, wsb, ids_big, b_ids, b_ln, b_out, b_tok
+    res["k5_shard_sort"] = bench_k5(args, lens, flush)
+    res["e2e"] = bench_presort_e2e(args, lens, pools[48])
     return res
+
+
+def bench_k5(args, lens, flush):
+    """K5 (device-wide stable radix sort + deal): every 1.25M-sample rank shard of the 10M corpus
+    sorted by (-length, id) in one call (north_star's per-rank radix sort on length keys),
+    (a) ids in shard order (the stratified shard: the id digits are skipped on the device) and
+    (b) ids shuffled inside each shard (every digit pass).  12 B/key algorithmic."""
+    import torch
+
+    import paper_2402_02447_b200 as B
+    from paper_2402_02447_b200.balance import presort_workspace_bytes
+
+    shard = CORPUS_N // SHARDS
+    d_len = torch.from_numpy(lens.astype(np.int32)).cuda()
+    rng = np.random.default_rng(5)
+    cases = {"ids_in_order": np.arange(CORPUS_N, dtype=np.int32),
+             "ids_shuffled": np.concatenate([rng.permutation(np.arange(r * shard, (r + 1) * shard, dtype=np.int32))
+                                             for r in range(SHARDS)])}
+    ws = torch.empty(presort_workspace_bytes(SHARDS, shard, 512, CORPUS_N - 1), dtype=torch.uint8, device="cuda")
+    hbm = peaks()["hbm_gbs"]
+    out = {}
+    for name, ids in cases.items():
+        d_ids = torch.from_numpy(ids).cuda()
+
+        def run():
+            return B.presort_deal(d_ids, d_len, shard, 1, "raster", max_len=512, max_id=CORPUS_N - 1,
+                                  workspace=ws)
+        r = run()
+        assert int(r[3]) == -1
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ts = []
+        for _ in range(max(3, min(args.steps, 10))):
+            flush.zero_()
+            ev[0].record()
+            run()
+            ev[1].record()
+            torch.cuda.synchronize()
+            ts.append(ev[0].elapsed_time(ev[1]))
+        ms = statistics.median(ts)
+        gbs = CORPUS_N * 12 / (ms * 1e-3) / 1e9
+        out[name] = {"ms": ms, "keys_per_s": CORPUS_N / (ms * 1e-3), "achieved_gbs": gbs, "frac": gbs / hbm,
+                     "bytes_per_key": 12}
+    out["config"] = "8 rank shards x 1.25M samples, one presort_deal(seg_len=1.25M, lanes=1) call, L2 flushed"
+    return out
+
+
+def bench_presort_e2e(args, lens, pool48):
+    """The batch former end to end through the public API with HOST buffers: host lengths and
+    host draws (an lb48 epoch of Topology(1,8) node steps) in, host stratum ids, dealt ids and
+    token counts out; every H2D / D2H inside the timed region (stratify_shards + presort_deal,
+    strata.py:61-83, balance.py:158-184)."""
+    import torch
+
+    import paper_2402_02447_b200 as B
+
+    ids, ln, steps = pool48
+    shard = CORPUS_N // SHARDS
+    offs = [r * shard for r in range(SHARDS + 1)]
+    h_lens = torch.from_numpy(lens.astype(np.int32)).pin_memory()
+    h_ids = torch.from_numpy(ids).pin_memory()
+    h_ln = torch.from_numpy(ln).pin_memory()
+    h_strata = torch.empty(CORPUS_N, dtype=torch.int32).pin_memory()
+    h_out = torch.empty(ids.size, dtype=torch.int32).pin_memory()
+    h_tok = torch.empty((steps, GPN), dtype=torch.int64).pin_memory()
+
+    def step():
+        st = B.stratify_shards(h_lens, offs, BOUNDS)  # H2D of the lengths, K2, shard counts to host
+        for r, ds in enumerate(st):
+            h_strata[offs[r]:offs[r + 1]].copy_(ds.ids, non_blocking=True)
+        d_ids = h_ids.to("cuda", non_blocking=True)
+        d_ln = h_ln.to("cuda", non_blocking=True)
+        out, tok, _, bad = B.presort_deal(d_ids, d_ln, GPN * 48, GPN, "snake", max_len=512, max_id=CORPUS_N - 1)
+        h_out.copy_(out.view(-1), non_blocking=True)
+        h_tok.copy_(tok, non_blocking=True)
+        torch.cuda.synchronize()
+        return int(bad)
+
+    assert step() == -1
+    n = max(3, min(args.steps, 10))
+    t = time.perf_counter()
+    for _ in range(n):
+        step()
+    sec = (time.perf_counter() - t) / n
+    return {"value": CORPUS_N / sec, "unit": "keys/s", "ms_per_step": sec * 1e3, "steps": n,
+            "h2d_bytes_per_step": CORPUS_N * 4 + ids.size * 8, "d2h_bytes_per_step": CORPUS_N * 4 + ids.size * 4
+            + steps * GPN * 8,
+            "api": "stratify_shards(pinned host lengths) -> host stratum ids; presort_deal(host lb48 draws of a "
+                   "whole epoch) -> host dealt ids + token counts",
+            "keys": "10M samples stratified + 10M presorted and dealt per step"}
+
+
 
 
 def bench_mcsim(args, lens):
@@ -663,22 +778,47 @@ def blas_threads() -> int:
         return 1
 
 
-def cpu_clip_baseline(sample: np.ndarray, nb_total: int, reps: int = 3) -> dict:
+BERT_LARGE_DIM, BUCKET_ELEMS, BUCKET_SCALES = 335_141_888, 25 * 1024 * 1024 // 4, (1e-5, 1e-4, 1e-3)
+
+
+def host_bert_grads(seed: int = 2402, rank: int = 0):
+    """The H1 workload on the host (numpy only): BERT-large D fp32, 52 x 25 MiB buckets,
+    per-bucket scales drawn exactly like synthetic.bert_grads (same seed -> same scale per
+    bucket, so the same buckets clip); values are numpy normals, not the CUDA generator's."""
     from oracle import ddp_oracle as O
 
-    n = sample.size
-    # 8 copies of one 25 MiB bucket = 52.4M elements per rep (~1 s of reference work)
-    w = np.tile(sample.astype(np.float64), 8)[None, :]
-    layout = tuple((i * n, (i + 1) * n) for i in range(8))
-    limit_c = math.sqrt(8) / math.sqrt(nb_total)  # same per-bucket limit c/sqrt(52)
+    layout = O.capped_bucket_layout(BERT_LARGE_DIM, BUCKET_ELEMS)
+    scales = np.random.default_rng(seed + 7919 * rank).choice(np.asarray(BUCKET_SCALES), size=len(layout))
+    rng = np.random.default_rng(seed + rank)
+    g = np.empty(BERT_LARGE_DIM, np.float32)
+    for (a, b), sc in zip(layout, scales):
+        g[a:b] = rng.standard_normal(b - a, dtype=np.float32) * np.float32(sc)
+    return g, layout
+
+
+def reference_clip_step(workers_f32: np.ndarray, layout, threshold: float = 1.0):
+    """One reference-path step: GradientState(workers) (fp64 conversion + finiteness check,
+    gradsync.py:50,182-191) then sync_bucketwise (gradsync.py:148-162), as oracle restatements."""
+    from oracle import ddp_oracle as O
+
+    w = O.as_worker_matrix(workers_f32)
+    return O.sync_bucketwise(w, layout, threshold)
+
+
+def cpu_clip_baseline(reps: int = 2) -> dict:
+    """The reference CPU path on this host over the SAME workload as the GPU arm (full config)."""
+    g, layout = host_bert_grads()
+    reference_clip_step(g[None, :], layout)  # warm (page-in)
     times = []
     for _ in range(reps):
         t = time.perf_counter()
-        O.sync_bucketwise(w, layout, limit_c)
+        reference_clip_step(g[None, :], layout)
         times.append(time.perf_counter() - t)
     med = statistics.median(times)
-    return {"value": w.size * 4 / med / 1e9, "unit": "GB/s", "cores": blas_threads(), "kind": "port",
-            "sample": f"oracle sync_bucketwise (fp64, numpy), K=1, 8 x 25 MiB buckets ({w.size} elems), median of {reps}",
+    return {"value": g.size * 4 / med / 1e9, "unit": "GB/s", "cores": blas_threads(), "kind": "port",
+            "sample": f"full config: GradientState(fp32 (1, {g.size}) -> fp64) + sync_bucketwise over the 52 x 25 MiB "
+                      f"BERT-large buckets (oracle numpy restatement), median of {reps} steps",
+            "same_config": True, "seconds_per_step": med,
             "threads_note": "numpy elementwise ops single-threaded; the fp64 norm (BLAS ddot) uses `cores` threads",
             "host_cpus": len(os.sched_getaffinity(0))}
 
@@ -702,37 +842,49 @@ def cpu_presort_baseline(lens: np.ndarray, pools: dict) -> dict:
 
 # --------------------------------------------------------------------- reference arm
 def run_reference(args, rank, world):
+    """Reference arm: the reference CPU path (oracle restatement of gradsync/strata/balance;
+    /root/reference is not on the GPU box) on this host.  N=1: the full BERT-large config
+    every step.  N>1: K = N simulated workers (the reference's single-process form) over the
+    last ceil(52/N) buckets, so a step touches about D elements; declared as a sample."""
     if rank != 0:
         return None
-    from paper_2402_02447_b200 import synthetic
-
-    rng = np.random.default_rng(2402)
-    sample = (rng.standard_normal(synthetic.BERT_BUCKET_ELEMS if hasattr(synthetic, "BERT_BUCKET_ELEMS") else 6_553_600)
-              * 1e-4).astype(np.float32)
     from oracle import ddp_oracle as O
 
-    n = sample.size
-    w = np.tile(sample.astype(np.float64), 4)[None, :]
-    layout = tuple((i * n, (i + 1) * n) for i in range(4))
-    lim = 2.0 / math.sqrt(52)
-    for _ in range(args.warmup if args.warmup < 2 else 1):
-        O.sync_bucketwise(w, layout, lim)
+    g, layout = host_bert_grads()
+    nb = len(layout)
+    if world == 1:
+        w = g[None, :]
+        lay, thr, same = layout, 1.0, True
+        sample = "full config per step (K=1, 52 x 25 MiB buckets, GradientState fp64 conversion included)"
+    else:
+        nb_s = -(-nb // world)
+        sel = layout[nb - nb_s:]
+        a0 = sel[0][0]
+        lay = tuple((a - a0, b - a0) for a, b in sel)
+        # K workers: rank r's gradients are a rotated copy of the same buckets (distinct per worker)
+        w = np.stack([np.roll(g[a0:], 7919 * r) for r in range(world)])
+        thr = math.sqrt(nb_s) / math.sqrt(nb)  # the full config's per-bucket limit c/sqrt(52)
+        same = False
+        sample = (f"K={world} workers x the last {nb_s} of 52 buckets ({w.size} elements per step, "
+                  "GradientState fp64 conversion included)")
+    for _ in range(min(args.warmup, 1)):
+        reference_clip_step(w, lay, thr)
     t = time.perf_counter()
     for _ in range(args.steps):
-        O.sync_bucketwise(w, layout, lim)
-    s = (time.perf_counter() - t) / args.steps
-    v = w.size * 4 / s / 1e9
+        reference_clip_step(w, lay, thr)
+    sec = (time.perf_counter() - t) / args.steps
+    v = w.size * 4 / sec / 1e9
     lens, pools = reference_presort_inputs()
     pre = cpu_presort_baseline(lens, pools)
     return {
         "metric": "clip+allreduce GB/s", "value": v, "unit": "GB/s", "impl": "reference",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": s * 1e3,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": "BERT-large synthetic gradients, bucket-wise clip (25 MiB buckets, c/sqrt(52))",
-                   "sample": "4 x 25 MiB buckets per step (bounded sample), K=1"},
-        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": blas_threads(), "kind": "port",
-                         "sample": "oracle/ddp_oracle.sync_bucketwise (fp64 numpy), 4 x 25 MiB buckets per step",
+        "config": {"workload": "BERT-large synthetic gradients (D=335,141,888 fp32, 52 x 25 MiB buckets), "
+                               "bucket-wise clip c/sqrt(52) + average over workers",
+                   "sample": sample, "same_config": same},
+        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": blas_threads(), "kind": "port", "sample": sample,
                          "threads_note": "numpy elementwise single-threaded; BLAS ddot uses `cores` threads"},
         "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "presort": {"keys_per_s": pre["value"], "unit": "keys/s", "cpu_baseline": pre},
@@ -765,7 +917,6 @@ def main():
 
     rank, world, local = dist_init(args.gpus)
     r = bench_clip(args, rank, world, local)
-    sample = r.pop("_cpu_sample")
     bert = None
     if not args.no_bert:  # BERT-large MLPerf phase-2 step under the three clip disciplines (all ranks)
         try:
@@ -801,6 +952,8 @@ def main():
                        "l2": "inputs 1.34 GB/rank > 126 MB L2 (no flush needed)"},
             "roofline": r["roofline"], "e2e": r["e2e"], "gpu_launches": r["gpu_launches"], "clocks": r["clocks"],
         }
+        if "e2e_drop_in" in r:
+            line["e2e_drop_in"] = r["e2e_drop_in"]
         if "nvlink" in r:
             line["nvlink"] = r["nvlink"]
         if bert is not None:
@@ -812,7 +965,7 @@ def main():
         if mc is not None:
             line["mcsim"] = mc
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_clip_baseline(sample, 52)
+            line["cpu_baseline"] = cpu_clip_baseline()
             if presort is not None:
                 lens, pools, _ = presort_inputs()
                 line["presort"]["cpu_baseline"] = cpu_presort_baseline(lens, pools)

@@ -54,6 +54,7 @@ constexpr int RBITS = 9;           // widest digit
 constexpr int RBINS = 1 << RBITS;  // 512 bins
 constexpr int MAX_PASS = 8;
 constexpr int TOK_SMEM = 1024;     // lanes whose token sums are staged in shared memory
+constexpr int kLookBack = 16;      // predecessor status words per look-back round trip
 
 constexpr uint32_t ST_AGG = 1u << 30, ST_PRE = 2u << 30, ST_VAL = (1u << 30) - 1u;
 
@@ -182,9 +183,10 @@ __global__ void __launch_bounds__(RT) k_radix_upsweep(const __grid_constant__ Ra
 }
 
 // ---------------------------------------------------------------- onesweep pass
+template <bool POS>
 struct PassSmem {
   unsigned long long key[TILE];  // tile, digit-sorted
-  int32_t pos[TILE];
+  int32_t pos[POS ? TILE : 1];
   uint32_t whist[RW][RBINS];     // per-warp digit counts, then per-warp exclusive prefixes
   uint32_t off[RBINS];           // tile-local digit starts
   uint32_t gbase[RBINS];         // global (segment) offset of this tile's first key of each digit
@@ -196,7 +198,7 @@ struct PassSmem {
 template <bool POS>
 __global__ void __launch_bounds__(RT) k_radix_pass(const __grid_constant__ RadixParams p, int pass) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  PassSmem& sm = *reinterpret_cast<PassSmem*>(smem_raw);
+  PassSmem<POS>& sm = *reinterpret_cast<PassSmem<POS>*>(smem_raw);
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   if (t == 0) sm.tile = (int)atomicAdd(&p.counters[pass], 1u);
   __syncthreads();
@@ -282,19 +284,32 @@ __global__ void __launch_bounds__(RT) k_radix_pass(const __grid_constant__ Radix
   block_scan2(tot[0], tot[1], h0, h1, eloc, eglob, sm.warp_tot);
   sm.off[2 * t] = eloc;
   sm.off[2 * t + 1] = eloc + tot[0];
-  // decoupled look-back over the preceding tiles of this segment
+  // decoupled look-back over the preceding tiles of this segment, kLookBack
+  // predecessors per round trip (their status words are loaded together, then
+  // folded newest-first until an inclusive prefix is met; an unpublished
+  // word is re-polled on its own)
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int d = 2 * t + h;
     uint32_t excl = 0;
     if (tin > 0) {
+      const uint32_t* sp = p.status[pass & 1] + d;
       int64_t k = tile - 1;
-      while (true) {
-        const uint32_t v = ld_relaxed_u32(p.status[pass & 1] + (size_t)k * RBINS + d);
-        if ((v & ~ST_VAL) == 0u) continue;  // predecessor not published yet
-        excl += v & ST_VAL;
-        if (v & ST_PRE) break;
-        --k;
+      const int64_t kmin = tile - tin;  // first tile of the segment (always publishes ST_PRE)
+      bool done = false;
+      while (!done) {
+        uint32_t v[kLookBack];
+#pragma unroll
+        for (int u = 0; u < kLookBack; ++u) v[u] = k - u >= kmin ? ld_relaxed_u32(sp + (size_t)(k - u) * RBINS) : ST_PRE;
+#pragma unroll
+        for (int u = 0; u < kLookBack; ++u) {
+          if (done) break;
+          uint32_t x = v[u];
+          while ((x & ~ST_VAL) == 0u) x = ld_relaxed_u32(sp + (size_t)(k - u) * RBINS);  // not published yet
+          excl += x & ST_VAL;
+          if (x & ST_PRE) done = true;
+        }
+        k -= kLookBack;
       }
       st_relaxed_u32(&st[d], ST_PRE | (excl + tot[h]));
     }
@@ -330,19 +345,40 @@ __global__ void __launch_bounds__(RT) k_radix_pass(const __grid_constant__ Radix
   // last pass: deal straight from the sorted slot (balance.py:59-70)
   const unsigned long long idmask = (1ull << p.id_bits) - 1ull;
   const bool tok_smem = p.tokens && p.lanes <= TOK_SMEM;
-  for (int i = t; i < n; i += RT) {
-    const unsigned long long k = sm.key[i];
-    const uint32_t d = (uint32_t)(k >> shift) & mask;
-    const int64_t q = (int64_t)sm.gbase[d] + (i - sm.off[d]);  // sorted slot inside the segment
-    const int64_t r = q / p.lanes;
-    const int c = (int)(q - r * p.lanes);
-    const int ln = (p.snake && (r & 1)) ? p.lanes - 1 - c : c;  // balance.py:66-67
-    const int64_t o = sbase + (int64_t)ln * p.rows + r;
-    p.out_ids[o] = (int32_t)(k & idmask);
-    if (p.out_pos) p.out_pos[o] = sm.pos[i];
-    const int32_t len = p.max_len - (int32_t)(k >> p.id_bits);
-    if (tok_smem) atomicAdd(reinterpret_cast<unsigned long long*>(&sm.tok[ln]), (unsigned long long)len);
-    else if (p.tokens) atomicAdd(reinterpret_cast<unsigned long long*>(&p.tokens[seg * p.lanes + ln]), (unsigned long long)len);
+  // q / lanes = umul64hi(q, floor(2^64 / lanes) + 1), exact for q * lanes < 2^64
+  const unsigned long long lanes_magic = ~0ull / (unsigned long long)p.lanes + 1ull;
+  // lanes of a warp that deal to the same GPU lane add their lengths first (one atomic per
+  // group; with lanes = 1 every key of the tile lands on one counter)
+  const bool tok_redux = p.max_len < (1 << 26);
+  for (int i0 = 0; i0 < n; i0 += RT) {
+    const int i = i0 + t;
+    const bool v = i < n;
+    int ln = -1;
+    int32_t len = 0;
+    if (v) {
+      const unsigned long long k = sm.key[i];
+      const uint32_t d = (uint32_t)(k >> shift) & mask;
+      const int64_t q = (int64_t)sm.gbase[d] + (i - sm.off[d]);  // sorted slot inside the segment
+      const int64_t r = p.lanes == 1 ? q : (int64_t)__umul64hi((unsigned long long)q, lanes_magic);
+      const int c = (int)(q - r * p.lanes);
+      ln = (p.snake && (r & 1)) ? p.lanes - 1 - c : c;  // balance.py:66-67
+      const int64_t o = sbase + (int64_t)ln * p.rows + r;
+      p.out_ids[o] = (int32_t)(k & idmask);
+      if constexpr (POS) p.out_pos[o] = sm.pos[i];
+      len = p.max_len - (int32_t)(k >> p.id_bits);
+    }
+    if (!p.tokens) continue;
+    if (tok_redux) {
+      const unsigned grp = __match_any_sync(0xffffffffu, ln);
+      const unsigned sum = __reduce_add_sync(grp, (unsigned)len);
+      if (v && lane == __ffs(grp) - 1) {
+        if (tok_smem) atomicAdd(reinterpret_cast<unsigned long long*>(&sm.tok[ln]), (unsigned long long)sum);
+        else atomicAdd(reinterpret_cast<unsigned long long*>(&p.tokens[seg * p.lanes + ln]), (unsigned long long)sum);
+      }
+    } else if (v) {
+      if (tok_smem) atomicAdd(reinterpret_cast<unsigned long long*>(&sm.tok[ln]), (unsigned long long)len);
+      else atomicAdd(reinterpret_cast<unsigned long long*>(&p.tokens[seg * p.lanes + ln]), (unsigned long long)len);
+    }
   }
   if (tok_smem) {
     __syncthreads();
@@ -490,7 +526,7 @@ extern "C" int b2_presort_sort_deal(const int32_t* ids, const int32_t* lens, int
   const int64_t grid_up = (pl.ntiles + per - 1) / per;
   k_radix_upsweep<<<(unsigned)grid_up, RT, 0, st>>>(p, per);
   B2_CHECK(cudaGetLastError());
-  const size_t smem = sizeof(PassSmem);
+  const size_t smem = out_pos ? sizeof(PassSmem<true>) : sizeof(PassSmem<false>);
   static bool configured[64][2] = {};
   const bool pos = out_pos != nullptr;
   if (!configured[di.device & 63][pos]) {
