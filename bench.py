@@ -923,12 +923,17 @@ def main():
             from paper_2402_02447_b200.train_step import bert_large_step_bench
 
             bert = {}
-            for mode in ("stock", "after", "bucketwise"):
+            for mode in ("stock", "after", "bucketwise", "reducer", "presort"):
                 r_ = bert_large_step_bench(mode, steps=max(3, min(args.steps, 10)), warmup=2)
                 bert[mode] = {"samples_per_s": r_["samples_per_s"], "ms_per_step": r_["ms_per_step"]}
-                if "buckets" in r_:
-                    bert[mode]["buckets"] = r_["buckets"]
-            bert["config"] = "BertForPreTraining 336M (random init), seq 512, batch 48/GPU, bf16 autocast, AdamW, DDP 25 MiB buckets"
+                for k in ("buckets", "buckets_predicted_before_iter0", "buckets_ddp_after_rebuild", "comm_dtype",
+                          "batch_former"):
+                    if k in r_:
+                        bert[mode][k] = r_[k]
+            bert["config"] = ("BertForPreTraining 336M (random init), seq 512, batch 48/GPU, bf16 autocast, AdamW, "
+                              "25 MiB buckets; stock/after/bucketwise = DDP (fp32 allreduce), reducer = "
+                              "BucketwiseReducer (Algorithm 1, bf16 comm), presort = reducer + per-step batch former "
+                              "(K2 strata, native draws, LocalPresort/K3) inside the timed loop")
         except Exception as e:  # transformers missing etc.: report, do not fail the bench
             bert = {"error": str(e)[:200]}
     presort = None

@@ -1,13 +1,25 @@
 """BERT-large training step with the three clip disciplines.
 
 MLPerf BERT phase-2 shape: seq 512, local batch 48, bf16 autocast, fp32
-master gradients in DDP's 25 MiB buckets, AdamW.  Modes:
+master gradients in 25 MiB buckets, AdamW.  Modes:
   * ``stock``      — DDP allreduce, no clipping (speed ceiling);
   * ``after``      — DDP allreduce, then global-norm clip of the mean
                      (clip after allreduce, gradsync.py:131-134 semantics);
-  * ``bucketwise`` — the paper's method: DDP comm hook clips each bucket at
-                     c/sqrt(B) with K1 before its allreduce
-                     (sync_bucketwise, gradsync.py:148-162; Algorithm 1).
+  * ``bucketwise`` — DDP comm hook clips each DDP bucket at c/sqrt(B) with K1
+                     before its fp32 allreduce; B is DDP's rebuilt bucket
+                     count, predicted before iteration 0 from DDP's own
+                     assignment rule (first bucket 1 MiB, then 25 MiB, in
+                     backward order);
+  * ``reducer``    — the paper's Algorithm 1 without DDP: ``BucketwiseReducer``
+                     (own 25 MiB layout, B known up front, K1 clip + cast into
+                     a bf16 comm buffer as each bucket's gradients land,
+                     ncclAllReduce on a side stream, overlapped with backward);
+  * ``presort``    — ``reducer`` fed by the paper's batch former every step:
+                     per-rank stratified draws (NativeDraws, strata.py:113-161)
+                     from a K2-stratified rank shard of the 10M Wikipedia-like
+                     corpus, the node's local presort (LocalPresort: all-gather
+                     + K3, balance.py:158-184), the dealt samples' lengths as
+                     the attention masks (config 4 of BASELINE.json).
 Synthetic token ids and random-init weights (no network).  Returns
 samples/s over the timed steps (CUDA events, max over ranks).
 """
@@ -20,15 +32,18 @@ import os
 import torch
 import torch.distributed as dist
 
+import numpy as np
+
 from .ddp import bucketwise_clip_hook, make_hook_state
 from .gradsync import ClipConfig
+from .reducer import BucketwiseReducer
 
 BERT_LARGE = dict(vocab_size=30528, hidden_size=1024, num_hidden_layers=24, num_attention_heads=16,
                   intermediate_size=4096, max_position_embeddings=512)
 
 
-def _batch(batch: int, seq: int, device, gen):
-    ids = torch.randint(0, BERT_LARGE["vocab_size"], (batch, seq), device=device, generator=gen)
+def _batch(batch: int, seq: int, device, gen, vocab: int = BERT_LARGE["vocab_size"]):
+    ids = torch.randint(0, vocab, (batch, seq), device=device, generator=gen)
     labels = torch.where(torch.rand(batch, seq, device=device, generator=gen) < 0.15, ids, torch.full_like(ids, -100))
     return {
         "input_ids": ids,
@@ -39,8 +54,62 @@ def _batch(batch: int, seq: int, device, gen):
     }
 
 
+def ddp_bucket_count(model, bucket_cap_mb: int = 25) -> int:
+    """B of DDP's buckets after its iteration-1 rebuild, computed before iteration 0: DDP's own
+    assignment rule (torch.distributed._compute_bucket_assignment_by_size with the 1 MiB first
+    bucket and the cap) over the parameters in backward order (reverse registration order)."""
+    params = [p for p in model.parameters() if p.requires_grad]
+    rev = list(reversed(params))
+    buckets, _ = dist._compute_bucket_assignment_by_size(
+        rev, [dist._DEFAULT_FIRST_BUCKET_BYTES, bucket_cap_mb * 1024 * 1024], [False] * len(rev))
+    return len(buckets)
+
+
+class PresortBatches:
+    """The paper's batch former on the device path, one local batch per step for this rank.
+
+    Rank r of a Topology(1, gpus) node owns the contiguous shard r of the corpus;
+    its strata come from K2 (stratify_lengths), each step draws ``lb`` samples
+    with seed derive_seed(seed, r, step) (NativeDraws, bit-exact draw_batch),
+    LocalPresort all-gathers the node's draws and deals them with K3, and the
+    rank's dealt lengths become the batch's attention mask.
+    """
+
+    def __init__(self, lengths: np.ndarray, local_batch: int, seq: int, seed: int = 2402):
+        from .presort_dist import LocalPresort
+        from .seqdata import Topology
+        from .strata import NativeDraws, allocate_counts, stratify_lengths
+
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        n = lengths.size // self.world
+        off = self.rank * n
+        shard = np.ascontiguousarray(lengths[off:off + n], dtype=np.int32)
+        ds = stratify_lengths(shard)  # K2
+        o = np.concatenate([[0], np.cumsum(ds.counts)])
+        ids = ds.ids.cpu().numpy().astype(np.int64) + off
+        self.nd = NativeDraws([ids[o[k]:o[k + 1]] for k in range(len(ds.counts))], ds.boundaries)
+        self.counts = allocate_counts(ds.probs, local_batch).counts
+        self.lengths = lengths
+        self.d_lengths = torch.from_numpy(np.ascontiguousarray(lengths, dtype=np.int32)).cuda()
+        self.lp = LocalPresort(Topology(1, self.world), local_batch, int(lengths.max()), int(lengths.size - 1))
+        self.seed, self.seq, self.step_i = seed, seq, 0
+        self.pos = torch.arange(seq, device="cuda")
+
+    def next(self):
+        from .strata import derive_seed
+
+        ids = self.nd.draw(self.counts, derive_seed(self.seed, self.rank, self.step_i))
+        self.step_i += 1
+        d_ids = torch.from_numpy(ids.astype(np.int32)).cuda(non_blocking=True)
+        d_len = torch.from_numpy(self.lengths[ids].astype(np.int32)).cuda(non_blocking=True)
+        mine, tokens = self.lp.step(d_ids, d_len)
+        lens = self.d_lengths[mine.long()].clamp(max=self.seq)
+        return (self.pos[None, :] < lens[:, None]).long(), tokens
+
+
 def bert_large_step_bench(mode: str = "bucketwise", steps: int = 5, warmup: int = 2, batch: int = 48,
-                          seq: int = 512, clip: float = 1.0, bucket_cap_mb: int = 25) -> dict:
+                          seq: int = 512, clip: float = 1.0, bucket_cap_mb: int = 25, lengths=None,
+                          model_config: dict | None = None) -> dict:
     from torch.nn.parallel import DistributedDataParallel as DDP
     from transformers import BertConfig, BertForPreTraining
 
@@ -52,35 +121,54 @@ def bert_large_step_bench(mode: str = "bucketwise", steps: int = 5, warmup: int 
     dev = torch.device("cuda", torch.cuda.current_device())
     world = dist.get_world_size()
     torch.manual_seed(1234)
-    cfg = BertConfig(**BERT_LARGE)
+    cfg = BertConfig(**(model_config or BERT_LARGE))
     cfg._attn_implementation = "sdpa"
     model = BertForPreTraining(cfg).to(dev)
-    ddp = DDP(model, device_ids=[dev.index], bucket_cap_mb=bucket_cap_mb, gradient_as_bucket_view=True)
-    state = None
-    if mode == "bucketwise":
-        n_params = sum(p.numel() for p in model.parameters())
-        guess = max(1, math.ceil(n_params * 4 / (bucket_cap_mb * 1024 * 1024)))
-        state = make_hook_state(ClipConfig(clip, "bucket_wise"), guess)
-        ddp.register_comm_hook(state, bucketwise_clip_hook)
+    state = reducer = loader = None
+    predicted = None
+    if mode in ("stock", "after", "bucketwise"):
+        ddp = DDP(model, device_ids=[dev.index], bucket_cap_mb=bucket_cap_mb, gradient_as_bucket_view=True)
+        if mode == "bucketwise":
+            predicted = ddp_bucket_count(model, bucket_cap_mb)  # B before iteration 0
+            state = make_hook_state(ClipConfig(clip, "bucket_wise"), predicted)
+            ddp.register_comm_hook(state, bucketwise_clip_hook)
+    elif mode in ("reducer", "presort"):
+        ddp = model
+        reducer = BucketwiseReducer(model.parameters(), ClipConfig(clip, "bucket_wise"), bucket_cap_mb=bucket_cap_mb)
+        if mode == "presort":
+            if lengths is None:
+                from .seqdata import LengthDistribution, generate_lengths
+
+                lengths = generate_lengths(LengthDistribution(), 10_000_000, 2402)
+            loader = PresortBatches(lengths, batch, seq)
+    else:
+        raise ValueError(f"unknown mode {mode!r}")
     opt = torch.optim.AdamW(model.parameters(), lr=1e-4, fused=True)
     gen = torch.Generator(device=dev)
     gen.manual_seed(7 + dist.get_rank())
-    data = _batch(batch, seq, dev, gen)
+    data = _batch(batch, seq, dev, gen, cfg.vocab_size)
 
     def step():
+        if loader is not None:  # this step's presorted local batch: its lengths mask the tokens
+            mask, _tok = loader.next()
+            data["attention_mask"] = mask
         with torch.autocast("cuda", dtype=torch.bfloat16):
             loss = ddp(**data).loss
         loss.backward()
+        if reducer is not None:
+            reducer.finish(check_finite=False)  # flags checked once after the timed loop
         if mode == "after":
             torch.nn.utils.clip_grad_norm_(model.parameters(), clip)
         opt.step()
-        opt.zero_grad(set_to_none=False)
+        if reducer is not None:
+            reducer.zero_grad()
+        else:
+            opt.zero_grad(set_to_none=False)
         return loss
 
     for _ in range(warmup):
         step()
-    if state is not None:  # DDP rebuilt its buckets after iteration 1: fix B = c/sqrt(B)'s B
-        state.set_num_buckets(max(state.norms) + 1 if state.norms else 1)
+    actual = (max(state.norms) + 1 if state.norms else 1) if state is not None else None
     torch.cuda.synchronize()
     dist.barrier()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -96,6 +184,16 @@ def bert_large_step_bench(mode: str = "bucketwise", steps: int = 5, warmup: int 
            "batch_per_gpu": batch, "seq": seq, "loss": float(loss), "params": sum(p.numel() for p in model.parameters())}
     if state is not None:
         out["buckets"] = state.num_buckets
-    del ddp, model, opt
+        out["buckets_predicted_before_iter0"] = predicted
+        out["buckets_ddp_after_rebuild"] = actual
+    if reducer is not None:
+        if bool(reducer.nonfinite.any()):
+            raise ValueError("gradient has non-finite components")
+        out["buckets"] = len(reducer.layout)
+        out["comm_dtype"] = str(reducer.comm.dtype).replace("torch.", "")
+        reducer.remove()
+    if loader is not None:
+        out["batch_former"] = "K2 strata + NativeDraws + LocalPresort (all-gather + K3) every step"
+    del ddp, model, opt, reducer, loader
     torch.cuda.empty_cache()
     return out
