@@ -926,8 +926,8 @@ def main():
             for mode in ("stock", "after", "bucketwise", "reducer", "presort"):
                 r_ = bert_large_step_bench(mode, steps=max(3, min(args.steps, 10)), warmup=2)
                 bert[mode] = {"samples_per_s": r_["samples_per_s"], "ms_per_step": r_["ms_per_step"]}
-                for k in ("buckets", "buckets_predicted_before_iter0", "buckets_ddp_after_rebuild", "comm_dtype",
-                          "batch_former"):
+                for k in ("buckets", "buckets_iter0", "buckets_after_rebuild", "comm_dtype", "batch_former",
+                          "batch_former_ms_per_step", "same_mask_without_former_ms_per_step"):
                     if k in r_:
                         bert[mode][k] = r_[k]
             bert["config"] = ("BertForPreTraining 336M (random init), seq 512, batch 48/GPU, bf16 autocast, AdamW, "

@@ -38,7 +38,7 @@ class LocalPresort:
     """Per-step (or per-epoch) local presort of this node's draws; returns this rank's lane."""
 
     def __init__(self, topo: Topology, local_batch: int, max_len: int, max_id: int,
-                 scan: ScanPattern | str = ScanPattern.SNAKE, group=None, deal=None):
+                 scan: ScanPattern | str = ScanPattern.SNAKE, group=None, deal=None, deferred_check: bool = False):
         self.topo = topo
         self.lb = int(local_batch)
         self.max_len, self.max_id = int(max_len), int(max_id)
@@ -51,12 +51,25 @@ class LocalPresort:
         # deal(ids, lens, seg_len, lanes, scan) -> (out[nseg, lanes, rows], tokens[nseg, lanes]);
         # K3 by default, replaceable for CPU tests
         self.deal = deal if deal is not None else self._k3
+        # deferred_check: keep K3's bad-sample index on the device (no host sync per step, so the
+        # host keeps running ahead of the GPU); check() raises for every step since the last check
+        self.deferred = bool(deferred_check)
+        self._bad = None
 
     def _k3(self, ids, lens, seg_len, lanes, scan):
         out, tok, _, bad = presort_deal(ids, lens, seg_len, lanes, scan, max_len=self.max_len, max_id=self.max_id)
-        if int(bad) >= 0:
+        if self.deferred:
+            self._bad = bad.clone() if self._bad is None else torch.maximum(self._bad, bad)
+        elif int(bad) >= 0:
             raise ValueError(f"sample at flat pool index {int(bad)} has length/id outside the declared range")
         return out, tok
+
+    def check(self) -> None:
+        """Raise if any deal since the last check met a sample outside the declared range (deferred mode)."""
+        if self._bad is not None:
+            bad, self._bad = int(self._bad.item()), None
+            if bad >= 0:
+                raise ValueError("a presorted sample has length/id outside the declared range")
 
     def _gather(self, mine: torch.Tensor) -> torch.Tensor:
         """[gpn, *mine.shape] of every node rank's tensor, in GPU order (balance.py:180-182)."""

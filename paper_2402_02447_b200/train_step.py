@@ -28,6 +28,7 @@ from __future__ import annotations
 
 import math
 import os
+import time
 
 import torch
 import torch.distributed as dist
@@ -54,14 +55,28 @@ def _batch(batch: int, seq: int, device, gen, vocab: int = BERT_LARGE["vocab_siz
     }
 
 
-def ddp_bucket_count(model, bucket_cap_mb: int = 25) -> int:
-    """B of DDP's buckets after its iteration-1 rebuild, computed before iteration 0: DDP's own
-    assignment rule (torch.distributed._compute_bucket_assignment_by_size with the 1 MiB first
-    bucket and the cap) over the parameters in backward order (reverse registration order)."""
-    params = [p for p in model.parameters() if p.requires_grad]
-    rev = list(reversed(params))
-    buckets, _ = dist._compute_bucket_assignment_by_size(
-        rev, [dist._DEFAULT_FIRST_BUCKET_BYTES, bucket_cap_mb * 1024 * 1024], [False] * len(rev))
+def ddp_bucket_counts(ddp, ready_order=None) -> int:
+    """B of DDP's bucket layout, from DDP's own assignment rule
+    (torch.distributed._compute_bucket_assignment_by_size with the size limits DDP passes it).
+    ready_order None: iteration 0's layout (registration order; with find_unused_parameters=False
+    DDP puts everything in ONE bucket for iteration 0).  Otherwise: the layout DDP rebuilds
+    before iteration 1 from the order gradients became ready in iteration 0."""
+    import sys
+
+    first = dist._DEFAULT_FIRST_BUCKET_BYTES if ddp.bucket_bytes_cap_default else ddp.bucket_bytes_cap
+    caps = list(getattr(ddp, "bucket_bytes_cap_list", None) or [])
+    if ready_order is None:
+        params = [p for p in ddp.module.parameters() if p.requires_grad]
+        if caps:
+            limits = caps
+        elif getattr(ddp, "static_graph", False) or not ddp.find_unused_parameters:
+            limits = [sys.maxsize]
+        else:
+            limits = [first, ddp.bucket_bytes_cap] if ddp.bucket_bytes_cap_default else [ddp.bucket_bytes_cap]
+    else:
+        params = list(ready_order)
+        limits = caps or [first, ddp.bucket_bytes_cap]
+    buckets, _ = dist._compute_bucket_assignment_by_size(params, limits, [False] * len(params))
     return len(buckets)
 
 
@@ -91,18 +106,31 @@ class PresortBatches:
         self.counts = allocate_counts(ds.probs, local_batch).counts
         self.lengths = lengths
         self.d_lengths = torch.from_numpy(np.ascontiguousarray(lengths, dtype=np.int32)).cuda()
-        self.lp = LocalPresort(Topology(1, self.world), local_batch, int(lengths.max()), int(lengths.size - 1))
+        self.lp = LocalPresort(Topology(1, self.world), local_batch, int(lengths.max()), int(lengths.size - 1),
+                               deferred_check=True)
         self.seed, self.seq, self.step_i = seed, seq, 0
         self.pos = torch.arange(seq, device="cuda")
+        # pinned staging ring: the H2D of step t is truly asynchronous, and slot t is rewritten
+        # only after its copy has run (event), so the host never waits on the GPU queue
+        self.ring = [torch.empty((2, local_batch), dtype=torch.int32).pin_memory() for _ in range(4)]
+        self.ring_ev = [None] * len(self.ring)
 
     def next(self):
         from .strata import derive_seed
 
         ids = self.nd.draw(self.counts, derive_seed(self.seed, self.rank, self.step_i))
+        slot = self.step_i % len(self.ring)
         self.step_i += 1
-        d_ids = torch.from_numpy(ids.astype(np.int32)).cuda(non_blocking=True)
-        d_len = torch.from_numpy(self.lengths[ids].astype(np.int32)).cuda(non_blocking=True)
-        mine, tokens = self.lp.step(d_ids, d_len)
+        if self.ring_ev[slot] is not None:
+            self.ring_ev[slot].synchronize()
+        h = self.ring[slot].numpy()
+        h[0] = ids
+        h[1] = self.lengths[ids]
+        d = self.ring[slot].to("cuda", non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self.ring_ev[slot] = ev
+        mine, tokens = self.lp.step(d[0], d[1])
         lens = self.d_lengths[mine.long()].clamp(max=self.seq)
         return (self.pos[None, :] < lens[:, None]).long(), tokens
 
@@ -129,9 +157,12 @@ def bert_large_step_bench(mode: str = "bucketwise", steps: int = 5, warmup: int 
     if mode in ("stock", "after", "bucketwise"):
         ddp = DDP(model, device_ids=[dev.index], bucket_cap_mb=bucket_cap_mb, gradient_as_bucket_view=True)
         if mode == "bucketwise":
-            predicted = ddp_bucket_count(model, bucket_cap_mb)  # B before iteration 0
+            params = [p for p in model.parameters() if p.requires_grad]
+            predicted = ddp_bucket_counts(ddp)  # iteration 0's B, before it runs
             state = make_hook_state(ClipConfig(clip, "bucket_wise"), predicted)
             ddp.register_comm_hook(state, bucketwise_clip_hook)
+            ready: list = []  # gradient-ready order of iteration 0 = DDP's rebuilt bucket order
+            recorders = [p.register_post_accumulate_grad_hook(lambda q: ready.append(q)) for p in params]
     elif mode in ("reducer", "presort"):
         ddp = model
         reducer = BucketwiseReducer(model.parameters(), ClipConfig(clip, "bucket_wise"), bucket_cap_mb=bucket_cap_mb)
@@ -166,9 +197,19 @@ def bert_large_step_bench(mode: str = "bucketwise", steps: int = 5, warmup: int 
             opt.zero_grad(set_to_none=False)
         return loss
 
-    for _ in range(warmup):
+    actual = actual0 = rebuilt = None
+    for i in range(warmup):
         step()
-    actual = (max(state.norms) + 1 if state.norms else 1) if state is not None else None
+        if state is not None and i == 0:
+            # DDP rebuilds its buckets before iteration 1: set B for the rebuilt layout now
+            actual0 = max(state.norms) + 1 if state.norms else 1
+            for h in recorders:
+                h.remove()
+            rebuilt = ddp_bucket_counts(ddp, ready)
+            state.set_num_buckets(rebuilt)
+            state.norms.clear()
+    if state is not None:
+        actual = max(state.norms) + 1 if state.norms else 1
     torch.cuda.synchronize()
     dist.barrier()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -181,11 +222,11 @@ def bert_large_step_bench(mode: str = "bucketwise", steps: int = 5, warmup: int 
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     out = {"mode": mode, "ms_per_step": ms, "samples_per_s": world * batch / (ms * 1e-3), "world": world,
-           "batch_per_gpu": batch, "seq": seq, "loss": float(loss), "params": sum(p.numel() for p in model.parameters())}
+           "batch_per_gpu": batch, "seq": seq, "loss": float(loss.detach()), "params": sum(p.numel() for p in model.parameters())}
     if state is not None:
         out["buckets"] = state.num_buckets
-        out["buckets_predicted_before_iter0"] = predicted
-        out["buckets_ddp_after_rebuild"] = actual
+        out["buckets_iter0"] = {"predicted": predicted, "ddp": actual0}
+        out["buckets_after_rebuild"] = {"predicted": rebuilt, "ddp": actual}
     if reducer is not None:
         if bool(reducer.nonfinite.any()):
             raise ValueError("gradient has non-finite components")
@@ -193,6 +234,29 @@ def bert_large_step_bench(mode: str = "bucketwise", steps: int = 5, warmup: int 
         out["comm_dtype"] = str(reducer.comm.dtype).replace("torch.", "")
         reducer.remove()
     if loader is not None:
+        # the batch former alone (host draws + H2D + all-gather + K3 + mask), per step
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(20):
+            loader.next()
+        torch.cuda.synchronize()
+        out["batch_former_ms_per_step"] = (time.perf_counter() - t0) / 20 * 1e3
+        # the same step with this step's padding mask held fixed (no batch former): the mask, not
+        # the former, is what changes the attention kernels' cost
+        fixed = data["attention_mask"].clone()
+        loader_saved, loader = loader, None
+        for _ in range(2):
+            step()
+        torch.cuda.synchronize()
+        a.record()
+        for _ in range(steps):
+            step()
+        b.record()
+        torch.cuda.synchronize()
+        out["same_mask_without_former_ms_per_step"] = a.elapsed_time(b) / steps
+        loader = loader_saved
+        del fixed
+        loader.lp.check()
         out["batch_former"] = "K2 strata + NativeDraws + LocalPresort (all-gather + K3) every step"
     del ddp, model, opt, reducer, loader
     torch.cuda.empty_cache()

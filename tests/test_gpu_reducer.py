@@ -95,6 +95,7 @@ def test_train_step_modes_small_bert(mode):
                               model_config=small)
     assert np.isfinite(r["loss"]) and r["samples_per_s"] > 0
     if mode == "bucketwise":
-        assert r["buckets_predicted_before_iter0"] == r["buckets_ddp_after_rebuild"]
+        assert r["buckets_iter0"]["predicted"] == r["buckets_iter0"]["ddp"]
+        assert r["buckets_after_rebuild"]["predicted"] == r["buckets_after_rebuild"]["ddp"]
     else:
         assert r["buckets"] >= 2
