@@ -368,3 +368,37 @@ def test_state_construction_kats():
         else:
             ref = O.sync_bucketwise(W, ((0, 2), (2, 4)), 1.0)
         np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-15)
+
+
+@pytest.mark.parametrize("n", [606_209, 6_553_600, 6_553_600 + 3, 13_000_001])
+@pytest.mark.parametrize("shift", [0, 1])
+@pytest.mark.parametrize("scale", [1e-5, 1e-3, 1e25])
+def test_lone_bucket_hook_shape(n, shift, scale):
+    """A lone bucket per launch (the DDP-hook / reducer shape, the L2-lag K1 over the full grid):
+    norms, coefficient and clipped values vs the oracle, fp32 and bf16 out, 16 B-misaligned heads
+    (shift) and ragged tails, below/above the limit and fp32-overflowing squares; bit-identical on
+    repeat; a NaN raises the bucket's non-finite flag."""
+    rng = np.random.default_rng(n + shift)
+    x = (rng.normal(size=n + shift) * scale).astype(np.float32)
+    g = torch.from_numpy(x).cuda()[shift:]
+    gh = x[shift:].astype(np.float64)
+    c = BucketClipper()
+    lim = 0.5
+    rn, rc = O.bucket_coefficients(gh, [(0, n)], lim)
+    for odt in (torch.float32, torch.bfloat16):
+        out = torch.empty(n + 1, dtype=odt, device="cuda")[shift:shift + n]
+        norms = torch.empty(1, dtype=torch.float64, device="cuda")
+        flags = torch.empty(1, dtype=torch.int32, device="cuda")
+        c.clip_cast(g, out, [(0, 0, n)], lim, norms=norms, nonfinite=flags)
+        np.testing.assert_allclose(norms.cpu().numpy(), rn, rtol=1e-6)
+        assert flags.item() == 0
+        tol = F32_REL if odt == torch.float32 else 2.0 ** -8
+        assert rel_err(out.float().cpu().numpy(), gh * rc[0]) <= tol
+        again = torch.empty_like(out)
+        c.clip_cast(g, again, [(0, 0, n)], lim)
+        assert torch.equal(again, out)
+    bad = g.clone()
+    bad[n // 3] = float("nan")
+    flags = torch.empty(1, dtype=torch.int32, device="cuda")
+    c.clip_cast(bad, torch.empty_like(bad), [(0, 0, n)], lim, nonfinite=flags)
+    assert flags.item() == 1
