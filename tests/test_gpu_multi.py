@@ -326,3 +326,51 @@ def test_fused_bert_large_streamed_equals_device_and_oracle():
         rows = np.stack([gs[r][a:b].astype(np.float64) for r in range(world)])
         ref = O.allreduce_mean(np.stack([O.clip_by_norm(row, limit) for row in rows]))
         assert np.abs(got - ref).max() <= 2.0 ** -7 * np.abs(ref).max()
+
+
+def _reducer_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    from paper_2402_02447_b200 import ClipConfig
+    from paper_2402_02447_b200.reducer import BucketwiseReducer
+
+    H.init(rank, world, port, "nccl")
+    try:
+        torch.manual_seed(0)  # identical init on every rank
+        m = torch.nn.Sequential(torch.nn.Linear(64, 300), torch.nn.GELU(), torch.nn.Linear(300, 512),
+                                torch.nn.GELU(), torch.nn.Linear(512, 10)).cuda()
+        g = torch.Generator(device="cuda").manual_seed(100 + rank)  # a different batch per rank
+        x = torch.randn(64, 64, device="cuda", generator=g)
+        y = torch.randint(0, 10, (64,), device="cuda", generator=g)
+        out = {}
+        for dt in (torch.float32, torch.bfloat16):
+            r = BucketwiseReducer(m.parameters(), ClipConfig(0.5, "bucket_wise"), bucket_cap_mb=0.1, comm_dtype=dt)
+            for p_ in m.parameters():  # this rank's own gradient (no reducer hooks)
+                p_.grad = None
+            r.remove()
+            loss = torch.nn.functional.cross_entropy(m(x), y)
+            raw = torch.cat([torch.autograd.grad(loss, p_, retain_graph=True)[0].reshape(-1) for p_ in m.parameters()])
+            r = BucketwiseReducer(m.parameters(), ClipConfig(0.5, "bucket_wise"), bucket_cap_mb=0.1, comm_dtype=dt)
+            torch.nn.functional.cross_entropy(m(x), y).backward()
+            r.finish()
+            out[str(dt)] = (raw.double().cpu().numpy(), r.flat.double().cpu().numpy(), r.layout)
+            r.remove()
+        torch.cuda.synchronize()
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bucketwise_reducer_nccl_matches_reference():
+    """BucketwiseReducer across ranks (rank r = worker row r): every rank ends with
+    sync_bucketwise of all ranks' gradients over the reducer's layout (gradsync.py:148-162)."""
+    from oracle import ddp_oracle as O
+
+    world = _world()
+    res = _run(_reducer_worker, world)
+    for dt, tol in ((str(torch.float32), 1e-5), (str(torch.bfloat16), 2.0 ** -7)):
+        W = np.stack([res[r][dt][0] for r in range(world)])
+        layout = res[0][dt][2]
+        ref = O.sync_bucketwise(W, layout, 0.5)
+        for r in range(world):
+            assert np.abs(res[r][dt][1] - ref).max() <= tol * np.abs(ref).max(), (dt, r)
