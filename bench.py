@@ -324,12 +324,32 @@ def bench_clip(args, rank, world, local):
         k1.record(compute)
         torch.cuda.synchronize()
         nccl_step_ms = max_over_ranks(k0.elapsed_time(k1) / args.steps, world)
+        # parity mode: K4 with an fp32 stage (the 1e-5 contract across ranks), same workload
+        f32_ms = None
+        if launches_per_step == 1:
+            try:
+                f32sync = FusedBucketSync(layout, cfg, transport="p2p", comm_dtype=torch.float32)
+                f32_replay, _ = capture(lambda s_: f32sync.sync(g, stream=s_))
+                for _ in range(3):
+                    f32_replay()
+                torch.cuda.synchronize()
+                barrier(world)
+                k0.record(compute)
+                for _ in range(args.steps):
+                    f32_replay()
+                k1.record(compute)
+                torch.cuda.synchronize()
+                f32_ms = max_over_ranks(k0.elapsed_time(k1) / args.steps, world)
+                f32sync.close()
+            except Exception as e:  # report, do not fail the bench
+                f32_ms = f"unavailable: {str(e)[:100]}"
         bus = lambda a: a * 2 * (world - 1) / world
         res["nvlink"] = {"algbw_gbs": algbw, "busbw_gbs": bus(algbw), "peak_gbs": 900.0,
                          "busbw_frac": bus(algbw) / 900.0, "peak_measured_gbs": 770.0,
                          "nccl_only_ms": nccl_ms, "nccl_only_busbw_gbs": bus(nccl_algbw),
                          "nccl_step_ms": nccl_step_ms, "speedup_vs_nccl_step": nccl_step_ms / ms,
                          "comm_dtype": "bf16",
+                         "fp32_parity_mode_ms": f32_ms,
                          "collective": (f"fused in K4 ({fsync.transport})" if launches_per_step == 1
                                         else "ncclAllReduce avg per 25 MiB bucket, side stream")}
         # roofline of the fused step (B200_PROFILING.md): bytes that must cross NVLink per

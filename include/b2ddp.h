@@ -158,6 +158,15 @@ int b2_bucket_clip_allreduce_p2p(const void* in, void* const* stages, uint32_t* 
                                  const int64_t* seg_off, const int64_t* seg_len, int nseg, double limit,
                                  double* norms, int32_t* nonfinite, void* workspace, size_t workspace_bytes,
                                  void* stream);
+/* The P2P form with a chosen stage dtype: B2_BF16 (the throughput form above)
+ * or B2_F32 — the parity mode: the clipped buckets are staged and averaged
+ * in fp32 (sum in fixed rank order, x 1/N), so the result meets the 1e-5
+ * relative contract of sync_bucketwise across ranks (gradsync.py:148-162)
+ * at twice the NVLink bytes.  stages[q] then hold D fp32 elements. */
+int b2_bucket_clip_allreduce_p2p_dtype(const void* in, void* const* stages, int stage_dtype, uint32_t* const* flags,
+                                       int nranks, int rank, const int64_t* seg_off, const int64_t* seg_len,
+                                       int nseg, double limit, double* norms, int32_t* nonfinite, void* workspace,
+                                       size_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------------------------------
  * H2 — stratified local presort

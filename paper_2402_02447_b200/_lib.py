@@ -47,6 +47,10 @@ SIGNATURES = {
         _I,
         [_P, _P, _P, _I, _I, _P, _P, _I, _D, _P, _P, _P, _SZ, _P],
     ),
+    "b2_bucket_clip_allreduce_p2p_dtype": (
+        _I,
+        [_P, _P, _I, _P, _I, _I, _P, _P, _I, _D, _P, _P, _P, _SZ, _P],
+    ),
     "b2_derive_seed": (C.c_uint64, [C.c_uint64, _P, _I]),
     "b2_draws_create": (_I, [C.POINTER(C.c_void_p), _P, _P, _I, _P]),
     "b2_draws_destroy": (_I, [_P]),

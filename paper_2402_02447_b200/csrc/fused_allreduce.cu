@@ -53,7 +53,7 @@ static double g_spin_timeout_s = -1.0;  // < 0: not yet read from the environmen
 
 struct FusedParams {
   ClipParams p;                        // in/out/limit/segments; p.out = local stage
-  __nv_bfloat16* stage[kMaxRanks];     // every rank's stage (index = rank)
+  void* stage[kMaxRanks];              // every rank's stage (index = rank): bf16, or fp32 (parity mode)
   uint32_t* flags[kMaxRanks];          // every rank's flag area [2][kMaxRanks][kMaxSegs]
   unsigned* pcount;                    // local arrival counters [2][kMaxSegs]
   unsigned* epoch;                     // launches so far (device; this launch is *epoch + 1)
@@ -141,10 +141,12 @@ __device__ __forceinline__ unsigned smid_u32() {
 // are settled by one registration barrier at entry (the launch is
 // cooperative, so every CTA is resident); chunks are derived from the actual
 // counts on the device.
-template <int kAT, int kBT, int UA, int UB, int UC, int RMAX, bool MC>
+template <int kAT, int kBT, int UA, int UB, int UC, int RMAX, bool MC, typename ST>
 __global__ void __launch_bounds__(kAT + kBT, 2) k_clip_allreduce_split(const __grid_constant__ FusedParams f) {
   using V = float4;
   constexpr int N = 4, kT = kAT + kBT;
+  constexpr int EPV = 16 / (int)sizeof(ST);  // stage elements per 16 B vector: 8 bf16 or 4 fp32
+  static_assert(!MC || sizeof(ST) == 2, "NVLS multimem reduce is built for the bf16 stage");
   const ClipParams& p = f.p;
   __shared__ double redA[32], redB[32];
   __shared__ double s_coef;
@@ -234,7 +236,7 @@ __global__ void __launch_bounds__(kAT + kBT, 2) k_clip_allreduce_split(const __g
     } else {
       const int gt = t - kAT;
       const uint64_t pol_drop = l2_policy_evict_first();
-      __nv_bfloat16* stage = f.stage[f.rank];
+      ST* stage = static_cast<ST*>(f.stage[f.rank]);
       for (int i = 0, s = gid; s < p.nseg; ++i, s += R) {
         if (gt == 0) {
           unsigned ns = 32;
@@ -265,7 +267,7 @@ __global__ void __launch_bounds__(kAT + kBT, 2) k_clip_allreduce_split(const __g
         const float cf = MC ? (float)(s_coef * (double)f.inv_n) : (float)s_coef;
         const Seg sg = p.seg[s];
         const float* in = static_cast<const float*>(p.in) + sg.in_off;
-        __nv_bfloat16* out = stage + sg.out_off;
+        ST* out = stage + sg.out_off;
         const V* vin = reinterpret_cast<const V*>(in + sg.head);
         const int64_t per = (sg.nv + G - 1) / G;
         const int64_t v0 = min64((int64_t)c * per, sg.nv), v1 = min64(v0 + per, sg.nv);
@@ -281,13 +283,13 @@ __global__ void __launch_bounds__(kAT + kBT, 2) k_clip_allreduce_split(const __g
             const int64_t vi = v + (int64_t)u * kBT;
             if (vi < v1) {
               float y[4] = {x[u].x * cf, x[u].y * cf, x[u].z * cf, x[u].w * cf};
-              put_vec<__nv_bfloat16, 4, float>(out + sg.head + vi * N, y);
+              put_vec<ST, 4, float>(out + sg.head + vi * N, y);
             }
           }
         }
         const int64_t tail0 = sg.head + sg.nv * N;
-        if (c == 0 && gt < sg.head) out[gt] = __float2bfloat16_rn(in[gt] * cf);
-        if (c == G - 1 && gt < sg.n - tail0) out[tail0 + gt] = __float2bfloat16_rn(in[tail0 + gt] * cf);
+        if (c == 0 && gt < sg.head) put1(out + gt, in[gt] * cf);
+        if (c == G - 1 && gt < sg.n - tail0) put1(out + tail0 + gt, in[tail0 + gt] * cf);
         group_sync<kBT>(kBarB);
         if (gt == 0) {
           __threadfence();
@@ -312,13 +314,13 @@ __global__ void __launch_bounds__(kAT + kBT, 2) k_clip_allreduce_split(const __g
       int64_t acc = 0;
       for (int s = 0; s < p.nseg; ++s) {
         const Seg sg = p.seg[s];
-        const int64_t nv8 = sg.n / 8;
-        const int64_t per_r = (nv8 + NR - 1) / NR;
-        const int64_t r0 = min64((int64_t)f.rank * per_r, nv8), r1 = min64(r0 + per_r, nv8);
+        const int64_t nvs = sg.n / EPV;  // 16 B stage vectors of the bucket
+        const int64_t per_r = (nvs + NR - 1) / NR;
+        const int64_t r0 = min64((int64_t)f.rank * per_r, nvs), r1 = min64(r0 + per_r, nvs);
         const int64_t per_c = (r1 - r0 + NC - 1) / NC;
         const int64_t c0 = min64(r0 + (int64_t)cidx * per_c, r1), c1 = min64(c0 + per_c, r1);
         s_beg[s] = acc;
-        s_voff[s] = sg.out_off / 8 + c0 - acc;
+        s_voff[s] = sg.out_off / EPV + c0 - acc;
         s_rdy[s] = 0u;
         acc += c1 - c0;
       }
@@ -379,19 +381,34 @@ __global__ void __launch_bounds__(kAT + kBT, 2) k_clip_allreduce_split(const __g
                        "f"(__uint_as_float(x[u][0].z)), "f"(__uint_as_float(x[u][0].w))
                        : "memory");
         } else {
-          float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          float acc[EPV];
+#pragma unroll
+          for (int i = 0; i < EPV; ++i) acc[i] = 0.f;
 #pragma unroll
           for (int q = 0; q < RMAX; ++q) {
             if (q < NR) {  // fixed rank order: identical bits on every rank
-              float e[8];
-              bf16x8_to_f32(x[u][q], e);
+              if constexpr (EPV == 8) {
+                float e[8];
+                bf16x8_to_f32(x[u][q], e);
 #pragma unroll
-              for (int i = 0; i < 8; ++i) acc[i] += e[i];
+                for (int i = 0; i < 8; ++i) acc[i] += e[i];
+              } else {
+                acc[0] += __uint_as_float(x[u][q].x);
+                acc[1] += __uint_as_float(x[u][q].y);
+                acc[2] += __uint_as_float(x[u][q].z);
+                acc[3] += __uint_as_float(x[u][q].w);
+              }
             }
           }
 #pragma unroll
-          for (int i = 0; i < 8; ++i) acc[i] *= f.inv_n;  // mean, not sum (gradsync.py:128)
-          const uint4 y = f32_to_bf16x8(acc);
+          for (int i = 0; i < EPV; ++i) acc[i] *= f.inv_n;  // mean, not sum (gradsync.py:128)
+          uint4 y;
+          if constexpr (EPV == 8) {
+            y = f32_to_bf16x8(acc);
+          } else {
+            y = make_uint4(__float_as_uint(acc[0]), __float_as_uint(acc[1]), __float_as_uint(acc[2]),
+                           __float_as_uint(acc[3]));
+          }
 #pragma unroll
           for (int q = 0; q < RMAX; ++q)
             if (q < NR) __stcg(reinterpret_cast<uint4*>(f.stage[q]) + vix[u], y);
@@ -429,9 +446,9 @@ __global__ void __launch_bounds__(kAT + kBT, 2) k_clip_allreduce_split(const __g
   }
 }
 
-template <int AT, int BT, int UA, int UB, int UC, int RMAX, bool MC = false>
+template <int AT, int BT, int UA, int UB, int UC, int RMAX, bool MC = false, typename ST = __nv_bfloat16>
 int launch_split(FusedParams& f, cudaStream_t stream, int comm_sms) {
-  auto kern = k_clip_allreduce_split<AT, BT, UA, UB, UC, RMAX, MC>;
+  auto kern = k_clip_allreduce_split<AT, BT, UA, UB, UC, RMAX, MC, ST>;
   const DeviceInfo& di = device_info();
   B2_REQUIRE(di.coop, B2_ERR_CUDA, "device does not support cooperative launch");
   static int occ_cached[64] = {};
@@ -527,7 +544,7 @@ extern "C" int b2_ipc_close(void* base) {
 static int clip_allreduce_impl(const void* in, void* const* stages, void* mc_stage, uint32_t* const* flags,
                                int nranks, int rank, const int64_t* seg_off, const int64_t* seg_len, int nseg,
                                double limit, double* norms, int32_t* nonfinite, void* workspace,
-                               size_t workspace_bytes, void* stream);
+                               size_t workspace_bytes, void* stream, int stage_dtype = B2_BF16);
 
 extern "C" int b2_bucket_clip_allreduce_nvls(const void* in, void* const* stages, void* mc_stage,
                                              uint32_t* const* flags, int nranks, int rank, const int64_t* seg_off,
@@ -548,10 +565,21 @@ extern "C" int b2_bucket_clip_allreduce_p2p(const void* in, void* const* stages,
                              nonfinite, workspace, workspace_bytes, stream);
 }
 
+extern "C" int b2_bucket_clip_allreduce_p2p_dtype(const void* in, void* const* stages, int stage_dtype,
+                                                  uint32_t* const* flags, int nranks, int rank,
+                                                  const int64_t* seg_off, const int64_t* seg_len, int nseg,
+                                                  double limit, double* norms, int32_t* nonfinite, void* workspace,
+                                                  size_t workspace_bytes, void* stream) {
+  B2_REQUIRE(stage_dtype == B2_BF16 || stage_dtype == B2_F32, B2_ERR_UNSUPPORTED,
+             "stage dtype must be B2_BF16 or B2_F32");
+  return clip_allreduce_impl(in, stages, nullptr, flags, nranks, rank, seg_off, seg_len, nseg, limit, norms,
+                             nonfinite, workspace, workspace_bytes, stream, stage_dtype);
+}
+
 static int clip_allreduce_impl(const void* in, void* const* stages, void* mc_stage, uint32_t* const* flags,
                                int nranks, int rank, const int64_t* seg_off, const int64_t* seg_len, int nseg,
                                double limit, double* norms, int32_t* nonfinite, void* workspace,
-                               size_t workspace_bytes, void* stream) {
+                               size_t workspace_bytes, void* stream, int stage_dtype) {
   B2_REQUIRE(in && stages && flags && seg_off && seg_len, B2_ERR_INVALID, "NULL argument");
   B2_REQUIRE(nranks >= 1 && nranks <= kMaxRanks && rank >= 0 && rank < nranks, B2_ERR_UNSUPPORTED,
              "nranks must be in [1, %d]", kMaxRanks);
@@ -565,13 +593,15 @@ static int clip_allreduce_impl(const void* in, void* const* stages, void* mc_sta
   for (int q = 0; q < nranks; ++q)
     B2_REQUIRE(reinterpret_cast<uintptr_t>(stages[q]) % 16 == 0, B2_ERR_INVALID, "stage %d not 16 B aligned", q);
   FusedParams f{};
-  int rc = fill_params(f.p, in, B2_F32, stages[rank], B2_BF16, seg_off, seg_off, seg_len, 0, nseg, limit, 1.0, norms,
-                       nullptr, nonfinite, workspace);
+  const bool f32 = stage_dtype == B2_F32;
+  B2_REQUIRE(!(f32 && mc_stage), B2_ERR_UNSUPPORTED, "the NVLS form reduces a bf16 stage");
+  int rc = fill_params(f.p, in, B2_F32, stages[rank], f32 ? B2_F32 : B2_BF16, seg_off, seg_off, seg_len, 0, nseg,
+                       limit, 1.0, norms, nullptr, nonfinite, workspace);
   if (rc != B2_OK) return rc;
   for (int s = 0; s < nseg; ++s)
     B2_REQUIRE(f.p.seg[s].vec, B2_ERR_UNSUPPORTED, "fused allreduce needs 16 B aligned gradients");
   for (int q = 0; q < nranks; ++q) {
-    f.stage[q] = static_cast<__nv_bfloat16*>(stages[q]);
+    f.stage[q] = stages[q];
     f.flags[q] = flags[q];
   }
   f.pcount = reinterpret_cast<unsigned*>(static_cast<char*>(workspace) + WsLayout::pcounters);
@@ -599,6 +629,11 @@ static int clip_allreduce_impl(const void* in, void* const* stages, void* mc_sta
     const int want = atoi(e);
     B2_REQUIRE(want == 2 || want == 4 || want == 8, B2_ERR_INVALID, "B2_K4_RMAX must be 2, 4 or 8");
     rmax = std::max(rmax, want);
+  }
+  if (f32) {  // parity mode: fp32 stage, the 1e-5 contract across ranks
+    if (rmax == 2) return launch_split<192, 320, 8, 4, 4, 2, false, float>(f, st, cs);
+    if (rmax == 4) return launch_split<192, 320, 8, 4, 2, 4, false, float>(f, st, cs);
+    return launch_split<192, 320, 8, 4, 1, 8, false, float>(f, st, cs);
   }
   if (rmax == 2) return launch_split<192, 320, 8, 4, 4, 2>(f, st, cs);
   if (rmax == 4) return launch_split<192, 320, 8, 4, 2, 4>(f, st, cs);

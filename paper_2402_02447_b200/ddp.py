@@ -253,7 +253,8 @@ class FusedBucketSync:
     gradient once the launch completes in stream order (graph-replayable).
     """
 
-    def __init__(self, layout: Sequence, cfg: ClipConfig, group=None, device=None, transport: str = "auto"):
+    def __init__(self, layout: Sequence, cfg: ClipConfig, group=None, device=None, transport: str = "auto",
+                 comm_dtype: torch.dtype = torch.bfloat16):
         if ClipConfig(cfg.threshold, cfg.mode).mode is not ClipMode.BUCKET_WISE:
             raise ValueError(f"config mode is {cfg.mode.value}, expected {ClipMode.BUCKET_WISE.value}")
         self.lib = _lib.load()
@@ -268,9 +269,17 @@ class FusedBucketSync:
             raise ValueError("fused sync supports up to 8 ranks")
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.dim = self.layout[-1][1]
-        stage_bytes = (self.dim * 2 + 255) // 256 * 256
+        if comm_dtype not in (torch.bfloat16, torch.float32):
+            raise ValueError("comm_dtype must be torch.bfloat16 or torch.float32")
+        self.comm_dtype = comm_dtype
+        esize = 2 if comm_dtype == torch.bfloat16 else 4
+        stage_bytes = (self.dim * esize + 255) // 256 * 256
         flag_bytes = self.lib.b2_p2p_flag_bytes()
         auto = transport == "auto"
+        if comm_dtype == torch.float32:  # parity mode: the fp32 stage is reduced two-shot over peer memory
+            if transport == "nvls":
+                raise ValueError("the NVLS form reduces a bf16 stage; use transport='p2p' for fp32")
+            transport, auto = "p2p", False
         if auto:  # NVLS cuts per-GPU NVLink traffic from 2(N-1)/N to 1 bucket: pays from N = 8
             transport = "nvls" if self.world >= 8 else "p2p"
         self._opened = []
@@ -311,7 +320,7 @@ class FusedBucketSync:
                     ptr = p.value
                 stages.append(ptr)
                 flags.append(ptr + stage_bytes)
-        self.stage = self.buf[: self.dim * 2].view(torch.bfloat16)
+        self.stage = self.buf[: self.dim * esize].view(comm_dtype)
         self._stages = (ctypes.c_void_p * self.world)(*stages)
         self._flags = (ctypes.c_void_p * self.world)(*flags)
         self.clipper = BucketClipper(device=self.device)
@@ -352,9 +361,10 @@ class FusedBucketSync:
                     grad.data_ptr(), self._stages, self.mc, self._flags, self.world, self.rank, offs, lens, n,
                     float(self.limit), self._norms_call[c0:].data_ptr(), None, ws.data_ptr(), ws.numel(), sp)
             else:
-                rc = self.lib.b2_bucket_clip_allreduce_p2p(
-                    grad.data_ptr(), self._stages, self._flags, self.world, self.rank, offs, lens, n,
-                    float(self.limit), self._norms_call[c0:].data_ptr(), None, ws.data_ptr(), ws.numel(), sp)
+                rc = self.lib.b2_bucket_clip_allreduce_p2p_dtype(
+                    grad.data_ptr(), self._stages, _DT[self.comm_dtype], self._flags, self.world, self.rank, offs,
+                    lens, n, float(self.limit), self._norms_call[c0:].data_ptr(), None, ws.data_ptr(), ws.numel(),
+                    sp)
             _lib.check(rc)
         return self.stage
 
@@ -372,7 +382,7 @@ class FusedBucketSync:
             raise ValueError(f"expected a host float32 gradient of {self.dim} elements")
         g = grad_host.reshape(-1)
         if out is None:
-            out = torch.empty(self.dim, dtype=torch.bfloat16, pin_memory=True)
+            out = torch.empty(self.dim, dtype=self.comm_dtype, pin_memory=True)
         if getattr(self, "_dev_in", None) is None:
             self._dev_in = torch.empty(self.dim, dtype=torch.float32, device=self.device)
             self._h2d, self._d2h = torch.cuda.Stream(self.device), torch.cuda.Stream(self.device)
@@ -392,9 +402,10 @@ class FusedBucketSync:
                     self._dev_in.data_ptr(), self._stages, self.mc, self._flags, self.world, self.rank, offs, lens,
                     n, float(self.limit), self._norms_call[c0:].data_ptr(), None, ws.data_ptr(), ws.numel(), sp)
             else:
-                rc = self.lib.b2_bucket_clip_allreduce_p2p(
-                    self._dev_in.data_ptr(), self._stages, self._flags, self.world, self.rank, offs, lens, n,
-                    float(self.limit), self._norms_call[c0:].data_ptr(), None, ws.data_ptr(), ws.numel(), sp)
+                rc = self.lib.b2_bucket_clip_allreduce_p2p_dtype(
+                    self._dev_in.data_ptr(), self._stages, _DT[self.comm_dtype], self._flags, self.world, self.rank,
+                    offs, lens, n, float(self.limit), self._norms_call[c0:].data_ptr(), None, ws.data_ptr(),
+                    ws.numel(), sp)
             _lib.check(rc)
             ev2 = torch.cuda.Event()
             ev2.record(compute)

@@ -124,3 +124,28 @@ def test_k4_rejects_bad_arguments():
         assert rc == _lib.B2_ERR_INVALID
     finally:
         del os.environ["B2_K4_RMAX"]
+
+
+@pytest.mark.parametrize("rmax", ["", "8"])
+def test_k4_fp32_stage_single_rank(rmax, monkeypatch):
+    """The parity-mode K4 (fp32 stage) at nranks = 1: within the 1e-5 fp32 contract of the oracle."""
+    if rmax:
+        monkeypatch.setenv("B2_K4_RMAX", rmax)
+    else:
+        monkeypatch.delenv("B2_K4_RMAX", raising=False)
+    gh = grads()
+    g = torch.from_numpy(gh).cuda()
+    k = Single(DIM, LAYOUT)
+    k.stage = torch.zeros(DIM, dtype=torch.float32, device="cuda")
+    k.stages = (ctypes.c_void_p * 1)(k.stage.data_ptr())
+    ref = O.sync_bucketwise(gh.astype(np.float64)[None, :], LAYOUT, 1.0)
+    for _ in range(2):
+        _lib.check(k.lib.b2_bucket_clip_allreduce_p2p_dtype(
+            g.data_ptr(), k.stages, _lib.B2_F32, k.flagp, 1, 0, k.offs, k.lens, len(LAYOUT), k.limit,
+            k.norms.data_ptr(), k.nonfinite.data_ptr(), k.ws.data_ptr(), k.ws.numel(), _lib.stream_ptr()))
+        out = k.stage.cpu().numpy()
+        assert np.abs(out - ref).max() <= 1e-5 * np.abs(ref).max()
+    rc = k.lib.b2_bucket_clip_allreduce_p2p_dtype(g.data_ptr(), k.stages, _lib.B2_F64, k.flagp, 1, 0, k.offs,
+                                                  k.lens, len(LAYOUT), k.limit, None, None, k.ws.data_ptr(),
+                                                  k.ws.numel(), None)
+    assert rc == _lib.B2_ERR_UNSUPPORTED

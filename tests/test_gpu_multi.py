@@ -374,3 +374,49 @@ def test_bucketwise_reducer_nccl_matches_reference():
         ref = O.sync_bucketwise(W, layout, 0.5)
         for r in range(world):
             assert np.abs(res[r][dt][1] - ref).max() <= tol * np.abs(ref).max(), (dt, r)
+
+
+def _fused_f32_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    from paper_2402_02447_b200 import ClipConfig
+    from paper_2402_02447_b200.ddp import FusedBucketSync
+
+    H.init(rank, world, port, "nccl")
+    try:
+        g = H.worker_grad(rank, DIM8).cuda()
+        sync = FusedBucketSync(LAYOUT8, ClipConfig(1.0, "bucket_wise"), transport="p2p", comm_dtype=torch.float32)
+        assert sync.stage.dtype == torch.float32
+        outs = [sync.sync(g).cpu().numpy() for _ in range(2)]
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=s):
+            sync.sync(g, stream=s)
+        graph.replay()
+        torch.cuda.synchronize()
+        outs.append(sync.stage.cpu().numpy())
+        outs.append(sync.sync_host(g.cpu().pin_memory(), chunk_buckets=2).numpy())
+        res = {"outs": outs, "norms": sync.norms.cpu().numpy()}
+        sync.close()
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_fused_clip_allreduce_fp32_parity_mode():
+    """K4 with an fp32 stage (b2_bucket_clip_allreduce_p2p_dtype, B2_F32): the fused multi-rank
+    path meets the 1e-5 fp32 contract of sync_bucketwise (gradsync.py:148-162), bit-identical
+    on every rank and every launch (device, graph replay, host-streamed)."""
+    from oracle import ddp_oracle as O
+
+    world = _world()
+    res = _run(_fused_f32_worker, world)
+    W = np.stack([H.worker_grad(r, DIM8).double().numpy() for r in range(world)])
+    ref = O.sync_bucketwise(W, LAYOUT8, 1.0)
+    scale = np.abs(ref).max()
+    first = res[0]["outs"][0]
+    for r in range(world):
+        for out in res[r]["outs"]:
+            assert np.abs(out - ref).max() <= 1e-5 * scale
+            np.testing.assert_array_equal(out, first)

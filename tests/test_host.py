@@ -27,7 +27,7 @@ def header_symbols():
 def test_library_exports_header_symbols():
     lib = _lib.load(require_device=False)
     syms = header_symbols()
-    assert len(syms) == 34, syms
+    assert len(syms) == 35, syms
     assert set(syms) == set(_lib.SIGNATURES), set(syms) ^ set(_lib.SIGNATURES)
     for s in syms:
         assert hasattr(lib, s), s
