@@ -13,7 +13,7 @@
 //   loads, L2 evict_last), B: scale pass over bucket s-1 (L2 re-read,
 //   evict_first) — so the grid-wide norm dependency of a bucket is hidden
 //   behind a whole bucket of A work.  Several buckets per launch: A and B are
-//   concurrent warp groups of every CTA (k_bucket_clip_ws, 192 + 320
+//   concurrent warp groups of every CTA (k_bucket_clip_ws, 256 + 256
 //   threads; small buckets form CTA groups, each owning every R-th bucket);
 //   a lone bucket (the DDP-hook shape): the time-sliced k_bucket_clip_l2lag.  Partials are published fire-and-forget
 //   and every CTA folds them in one fixed order (bit-deterministic, identical
@@ -506,15 +506,17 @@ int launch_ws(ClipParams& p, cudaStream_t stream) {
 
 // K1 configuration (tools/clip_bench.py sweeps; measurements in DESIGN.md):
 // several buckets per launch -> warp-specialised two-stream kernel
-// (192 norm + 320 scale threads, 2 CTAs/SM: the latency-bound L2 re-read
-// stream gets the larger group); a lone bucket (DDP-hook shape)
+// (256 norm + 256 scale threads, 8 vectors in flight per thread in both, 2
+// CTAs/SM: 375 us timed alone / 394 us at the power cap vs 382 / 401 for
+// round 1's 192 + 320 with 4 scale vectors, tools/step_timing_probe.py); a
+// lone bucket (DDP-hook shape)
 // -> the time-sliced L2-lag kernel, which has the shorter critical path.
 // (The measured alternatives — a TMA shared-memory ring and other warp
 // splits — live in git history, commit 4cd4b3b, not in the product library.)
 template <typename Tin, typename Tout>
 int launch_clip_k1(ClipParams& p, cudaStream_t stream) {
   // norm-only launches have no scale stream: the time-sliced kernel puts every thread on the norm
-  if (p.nseg >= 2 && p.out != nullptr) return launch_ws<Tin, Tout, 192, 320, 2, 1, 8, 4>(p, stream);
+  if (p.nseg >= 2 && p.out != nullptr) return launch_ws<Tin, Tout, 256, 256, 2, 1, 8, 8>(p, stream);
   return launch_l2lag<Tin, Tout, 384, 2, 1, 8, 4, 0>(p, stream);
 }
 

@@ -23,11 +23,15 @@ def rounds(n=10, k=20):
         out.append(a.elapsed_time(b) / k * 1e3)
     return [round(x, 1) for x in out]
 for _ in range(5): f()
-print("no sampler", rounds())
+import statistics
+r0 = rounds()
+print("no sampler", r0)
 with bench.ClockSampler(0) as clk:
     tl = time.perf_counter()
     while time.perf_counter() - tl < 0.6:
         f(); torch.cuda.synchronize()
-    print("sampler, after 0.6 s load", rounds())
+    r1 = rounds()
+    print("sampler, after 0.6 s load", r1)
 print(clk.summary())
 print("no sampler again", rounds())
+print("SUMMARY burst_median_us %.1f sustained_median_us %.1f" % (statistics.median(r0), statistics.median(r1)))
