@@ -402,3 +402,18 @@ def test_lone_bucket_hook_shape(n, shift, scale):
     flags = torch.empty(1, dtype=torch.int32, device="cuda")
     c.clip_cast(bad, torch.empty_like(bad), [(0, 0, n)], lim, nonfinite=flags)
     assert flags.item() == 1
+
+
+def test_gradient_state_staged_host_copy_is_exact():
+    """A large pageable numpy state goes to the device through the pinned staging ring
+    (gradsync._staged_h2d: several slots, host threads, ragged last slot): bit-exact copy,
+    and sync_bucketwise on it equals the oracle."""
+    rng = np.random.default_rng(8)
+    w = rng.standard_normal((2, 9_000_001)) * 1e-3  # 144 MB fp64: > 64 MB, several 8M-element slots
+    st = GradientState(w, equal_bucket_layout(w.shape[1], 5))
+    assert np.array_equal(st.workers.cpu().numpy(), w)
+    got = sync_bucketwise(st, BUCKET)
+    assert rel_err(got, O.sync_bucketwise(w, equal_bucket_layout(w.shape[1], 5), 1.0)) <= F64_REL
+    w32 = w[0].astype(np.float32)[None, :]
+    st32 = GradientState(torch.from_numpy(w32), equal_bucket_layout(w.shape[1], 5))  # fp32 tensor stays fp32
+    assert st32.workers.dtype == torch.float32 and np.array_equal(st32.workers.cpu().numpy(), w32)
