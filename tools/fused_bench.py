@@ -74,7 +74,11 @@ def main():
     if rank == 0:
         print(json.dumps({"world": world, "comm": args.comm, "cfg": os.environ.get("B2_FUSED_CFG", "0"), "bucket_mb": args.mb,
                           "buckets": len(layout), "ms": ms, "busbw_gbs": algbw * 2 * (world - 1) / world,
-                          "grad_gbs_per_rank": dim * 4 / (ms * 1e-3) / 1e9}), flush=True)
+                          "grad_gbs_per_rank": dim * 4 / (ms * 1e-3) / 1e9,
+                          # bytes each GPU must move per direction (two-shot 2(N-1)/N of the bf16
+                          # gradient, NVLS one copy) over the measured 770 GB/s peer copy
+                          "nvlink_roofline_frac": (dim * 2 * (1.0 if args.comm == "nvls" else 2 * (world - 1) / world)
+                                                   / 770e9 * 1e3) / ms}), flush=True)
     if hasattr(sync, "close"):
         sync.close()
     dist.destroy_process_group()
