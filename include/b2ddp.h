@@ -181,13 +181,16 @@ size_t b2_strata_workspace_bytes(int64_t n);
  * stratum, input order kept inside each stratum (:82).  `ids` may be NULL
  * (ids = 0..n-1).  Outputs (device): ids_out[n], counts[nb] (int64), and
  * bad[1] (int64) = first index i whose length is > bounds[nb-1] or < 1, or
- * -1 (so the wrapper raises naming that sample's id, :75-80).  `bounds` is
- * a [host] array of nb strictly ascending values >= 1, nb <= 16. */
+ * -1 (so the wrapper raises naming that sample's id, :75-80); when bad >= 0
+ * ids_out and counts are unspecified (the reference raises there).  `bounds`
+ * is a [host] array of nb strictly ascending values >= 1, nb <= 16.  Three
+ * launches: per-tile stratum codes + counts, a per-shard scan, the scatter
+ * (8.5 B/key of traffic for 8 B/key algorithmic). */
 int b2_strata_partition(const int32_t* lengths, const int32_t* ids, int64_t n,
                         const int32_t* bounds, int nb, int32_t* ids_out, int64_t* counts,
                         int64_t* bad, void* workspace, size_t workspace_bytes, void* stream);
 
-/* K2 over many rank shards in one pass (two launches in total): shard g is
+/* K2 over many rank shards in one pass (three launches in total): shard g is
  * lengths[shard_off[g] .. shard_off[g+1]) ([host] offsets, nshard <= 64) and
  * is stratified on its own, exactly like stratify() on that shard; ids_out
  * uses the same offsets, counts is [nshard][nb], bad[g] is the shard-local
