@@ -239,6 +239,22 @@ def bench_clip(args, rank, world, local):
         t1.record(compute)
         torch.cuda.synchronize()
         barrier(world)
+        sustained_copy = None
+        if world == 1:
+            # the copy peak in the same (power-capped) state: MEASURED_PEAKS' method (copy_ of
+            # 1 Gi bf16 elements, read + write bytes), right after the timed steps
+            src = torch.empty(1 << 30, dtype=torch.bfloat16, device="cuda")
+            dst = torch.empty_like(src)
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            best = None
+            for _ in range(5):
+                c0.record(compute)
+                dst.copy_(src)
+                c1.record(compute)
+                torch.cuda.synchronize()
+                best = min(best or 1e9, c0.elapsed_time(c1))
+            sustained_copy = 2 * src.numel() * 2 / (best * 1e-3) / 1e9
+            del src, dst
     ms = max_over_ranks(t0.elapsed_time(t1) / args.steps, world)
 
     # dominant kernel alone: the fused launch over all buckets, CUDA events on its stream
@@ -302,6 +318,8 @@ def bench_clip(args, rank, world, local):
                        "CUDA events over K launches of K1 alone (the step is K4)"),
             "burst": {"launch_us": kb_ms * 1e3, "achieved": kb_gbs, "frac": kb_gbs / pk["hbm_gbs"],
                       "note": "the same launch timed alone right after the step loop"},
+            "copy_peak_same_state_gbs": sustained_copy,
+            "frac_vs_copy_same_state": (step_gbs / sustained_copy) if sustained_copy else None,
             "per_bucket_launches": pb,
         },
         "gpu_launches": args.steps * launches_per_step,

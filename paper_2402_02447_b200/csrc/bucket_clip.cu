@@ -157,6 +157,7 @@ __global__ void __launch_bounds__(THREADS, CPS) k_bucket_clip_l2lag(const __grid
       if (__syncthreads_or(bad)) tot = __longlong_as_double(0x7ff8000000000000ll);  // NaN marks inf/nan input
     }
     if (t == 0) {
+      B2_DASSERT(s < kMaxSegs && c < G && (size_t)s * G + c < (size_t)kMaxSegs * kMaxGrid);
       p.partials[(size_t)s * G + c] = tot;
       red_release_u32(&p.counters[s], 1u);  // fire-and-forget arrival
     }
@@ -396,6 +397,7 @@ __global__ void __launch_bounds__(AT + BT, CPS) k_bucket_clip_ws(const __grid_co
       if constexpr (kF64) part = __any_sync(0xffffffffu, bad) ? __longlong_as_double(0x7ff8000000000000ll) : part;
       const double tot = group_sum<AT>(part, redA, gt, kBarA);  // NaN propagates: marks inf/nan input
       if (gt == 0) {
+        B2_DASSERT(s < kMaxSegs && c < kMaxGrid);
         p.partials[(size_t)s * kMaxGrid + c] = tot;
         red_release_u32(&p.counters[s], 1u);  // fire-and-forget arrival
       }

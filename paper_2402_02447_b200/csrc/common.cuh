@@ -43,6 +43,25 @@ inline int check_cuda(cudaError_t e, const char* what) {
     }                                \
   } while (0)
 
+// ---- device-side bounds checks (debug builds) -----------------------------
+// Built with -DB2_DEBUG_BOUNDS (tools/ab_build.sh debug ... with B2_NVCC_EXTRA),
+// every index of the hand-written shared/global protocols is checked and a
+// violation traps with its file:line; release builds compile the checks out.
+#ifdef B2_DEBUG_BOUNDS
+#define B2_DASSERT(cond)                                                          \
+  do {                                                                            \
+    if (!(cond)) {                                                                \
+      printf("B2_DASSERT %s:%d block %d thread %d: %s\n", __FILE__, __LINE__,    \
+             (int)blockIdx.x, (int)threadIdx.x, #cond);                           \
+      __trap();                                                                   \
+    }                                                                             \
+  } while (0)
+#else
+#define B2_DASSERT(cond) \
+  do {                   \
+  } while (0)
+#endif
+
 // ---- device-side primitives -------------------------------------------
 
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }

@@ -96,6 +96,8 @@ __device__ __forceinline__ void stamp(const ClipParams& p, int k) {
   if (p.nseg <= kMaxSegs - 8) reinterpret_cast<uint64_t*>(p.partials)[(size_t)(kMaxSegs - 1 - k) * kMaxGrid + blockIdx.x] = global_ns();
 }
 __device__ __forceinline__ uint32_t* flag(const FusedParams& f, int owner, int kind, int src, int s) {
+  B2_DASSERT(owner >= 0 && owner < f.nranks && kind >= 0 && kind < 2 && src >= 0 && src < kMaxRanks && s >= 0 &&
+             s < kMaxSegs);
   return f.flags[owner] + ((size_t)kind * kMaxRanks + src) * kMaxSegs + s;
 }
 
@@ -229,6 +231,7 @@ __global__ void __launch_bounds__(kAT + kBT, 2) k_clip_allreduce_split(const __g
         if (c == G - 1 && gt < sg.n - tail0) acc += (double)in[tail0 + gt] * in[tail0 + gt];
         const double tot = group_sum<kAT>(acc, redA, gt, kBarA);
         if (gt == 0) {
+          B2_DASSERT(s < kMaxSegs && c < kMaxGrid);
           p.partials[(size_t)s * kMaxGrid + c] = tot;
           red_release_u32(&p.counters[s], 1u);
         }

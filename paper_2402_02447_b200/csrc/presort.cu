@@ -244,6 +244,7 @@ __global__ void __launch_bounds__(32 * kCntWarps, MINB) k_presort_deal_count(con
         L = L < 1 ? 1 : (L > M ? M : L);  // keep the slot well-formed; the caller raises
       }
       const uint32_t bin = (uint32_t)(M - L), sh = (bin & 1u) << 4;
+      B2_DASSERT((int)(bin >> 1) < HW);
       const uint32_t old = atomicAdd(&hist[bin >> 1], 1u << sh);
       kb[j] = (bin << 16) | ((old >> sh) & 0xffffu);
       kd[j] = D;
@@ -305,12 +306,18 @@ __global__ void __launch_bounds__(32 * kCntWarps, MINB) k_presort_deal_count(con
       if (live(j)) {
         const uint32_t bin = kb[j] >> 16, rk = kb[j] & 0xffffu;
         const int pos = (int)(((hist[bin >> 1] >> ((bin & 1u) << 4)) & 0xffffu) + rk);
+        B2_DASSERT(pos >= 0 && pos < P);
         srt[pos] = kd[j];
-        if (rk == 1) smul[atomicAdd(&s_cnt[w][0], 1)] = (int16_t)bin;  // the bin holds 2+ keys
+        if (rk == 1) {  // the bin holds 2+ keys
+          const int q = atomicAdd(&s_cnt[w][0], 1);
+          B2_DASSERT(q < PM / 2);
+          smul[q] = (int16_t)bin;
+        }
         if (p.tokens) {  // the GPU lane slot `pos` is dealt to
           const int r = __float2int_rd(((float)pos + 0.5f) * inv_lanes), c = pos - r * lanes;
           const int g = (p.snake && (r & 1)) ? lanes - 1 - c : c;
           const int L = M - (int)bin;
+          B2_DASSERT(g >= 0 && g < lanes);
           if (tok_smem) atomicAdd(&stok[g], L);
           else atomicAdd(reinterpret_cast<unsigned long long*>(p.tokens + seg * lanes + g), (unsigned long long)L);
         }
@@ -324,7 +331,9 @@ __global__ void __launch_bounds__(32 * kCntWarps, MINB) k_presort_deal_count(con
     for (int q = lane; q < nmulti; q += 32) {
       const int b = smul[q], st = bstart(b), e = bstart(b + 1);
       if (e - st > kCntBig) {
-        smul[PM / 2 - 1 - atomicAdd(&s_cnt[w][1], 1)] = (int16_t)b;  // big list grows from the top
+        const int qb = PM / 2 - 1 - atomicAdd(&s_cnt[w][1], 1);  // big list grows from the top
+        B2_DASSERT(qb >= nmulti);
+        smul[qb] = (int16_t)b;
         continue;
       }
       for (int x = st + 1; x < e; ++x) {  // insertion sort, ids ascending
@@ -352,6 +361,7 @@ __global__ void __launch_bounds__(32 * kCntWarps, MINB) k_presort_deal_count(con
           const int32_t o = srt[y];
           f += (o < me) || (o == me && y < x);
         }
+        B2_DASSERT(f >= st && f < e);
         out[f] = me;
       }
       __syncwarp();
@@ -364,6 +374,7 @@ __global__ void __launch_bounds__(32 * kCntWarps, MINB) k_presort_deal_count(con
 #pragma unroll 4
     for (int o = lane; o < P; o += 32) {  // the deal as a gather (balance.py:59-70)
       const int c = (p.snake && (r & 1)) ? lanes - 1 - ln : ln;
+      B2_DASSERT(r < rows && c >= 0 && c < lanes && r * lanes + c < P);
       out[o] = srt[r * lanes + c];
       r += dr;
       ln += dq;

@@ -324,6 +324,7 @@ __global__ void __launch_bounds__(RT) k_radix_pass(const __grid_constant__ Radix
     if (i < n) {
       const uint32_t d = (uint32_t)(key[j] >> shift) & mask;
       const uint32_t lp = sm.off[d] + sm.whist[w][d] + rank[j];
+      B2_DASSERT(d < RBINS && lp < (uint32_t)n);
       sm.key[lp] = key[j];
       if constexpr (POS) sm.pos[lp] = pos[j];
     }
@@ -337,6 +338,7 @@ __global__ void __launch_bounds__(RT) k_radix_pass(const __grid_constant__ Radix
       const unsigned long long k = sm.key[i];
       const uint32_t d = (uint32_t)(k >> shift) & mask;
       const int64_t o = sbase + sm.gbase[d] + (i - sm.off[d]);
+      B2_DASSERT(o >= sbase && o < sbase + p.seg_len);
       kout[o] = k;
       if constexpr (POS) pout[o] = sm.pos[i];
     }
@@ -363,6 +365,7 @@ __global__ void __launch_bounds__(RT) k_radix_pass(const __grid_constant__ Radix
       const int c = (int)(q - r * p.lanes);
       ln = (p.snake && (r & 1)) ? p.lanes - 1 - c : c;  // balance.py:66-67
       const int64_t o = sbase + (int64_t)ln * p.rows + r;
+      B2_DASSERT(ln >= 0 && ln < p.lanes && r >= 0 && r < p.rows);
       p.out_ids[o] = (int32_t)(k & idmask);
       if constexpr (POS) p.out_pos[o] = sm.pos[i];
       len = p.max_len - (int32_t)(k >> p.id_bits);

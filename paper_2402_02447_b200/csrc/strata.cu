@@ -143,6 +143,7 @@ __global__ void __launch_bounds__(kT) k_strata_count(const __grid_constant__ Str
     // lanes QPW*m .. QPW*m + QPW-1 hold one word's quads
 #pragma unroll
     for (int o = 1; o < QPW; o <<= 1) packed |= __shfl_down_sync(0xffffffffu, packed, o) << (o * 4 * CB);
+    B2_DASSERT((i0 / 4) / QPW < WPT);
     if ((lane & (QPW - 1)) == 0) cw[(i0 / 4) / QPW] = packed;
   }
   if (CB == 2) c[0] -= c[1] + (NB > 2 ? c[2] : 0) + (NB > 3 ? c[3] : 0);
@@ -213,7 +214,8 @@ __global__ void __launch_bounds__(kScanT) k_strata_scan(const __grid_constant__ 
 // carries stratum k's next output slot (32-bit, within the shard).
 template <int NB, bool IDS, bool FULL>
 __device__ __forceinline__ void scatter_rounds(const StrataParams& p, const uint32_t (&word)[(kWarpKeys * code_bits<NB>() / 32) / 32],
-                                               int next, int32_t* out, const int32_t* ids, int wbase, int valid) {
+                                               int next, int32_t* out, const int32_t* ids, int wbase, int valid,
+                                               int shard_n) {
   constexpr int CB = code_bits<NB>();
   constexpr int WPL = (kWarpKeys * CB / 32) / 32;  // code words per lane (1 or 2)
   constexpr int KPW = 32 / CB;                     // keys per word
@@ -246,6 +248,7 @@ __device__ __forceinline__ void scatter_rounds(const StrataParams& p, const uint
       mk &= bits ^ inv[b];
     }
     const int base = __shfl_sync(0xffffffffu, next, code);
+    B2_DASSERT(!ok || (base + __popc(~diff & live & lt) >= 0 && base + __popc(~diff & live & lt) < shard_n));
     if (ok) out[base + __popc(~diff & live & lt)] = IDS ? __ldcs(ids + wbase + key) : wbase + key;
     next += __popc(mk);
   }
@@ -259,7 +262,7 @@ __device__ __forceinline__ void scatter_rounds(const StrataParams& p, const uint
 // ballots, scans or base updates.
 template <bool IDS, bool FULL>
 __device__ __forceinline__ void scatter_rounds_prefix(uint32_t word, const int* slot_tab, int32_t* out,
-                                                      const int32_t* ids, int wbase, int valid) {
+                                                      const int32_t* ids, int wbase, int valid, int shard_n) {
   constexpr uint32_t LOW = 0x55555555u;
   const int lane = threadIdx.x & 31;
   const int f = lane & 15, half = lane >> 4;
@@ -273,6 +276,7 @@ __device__ __forceinline__ void scatter_rounds_prefix(uint32_t word, const int* 
     const uint32_t y = wv ^ (LOW * code);
     const int inword = __popc(~(y | (y >> 1)) & below);
     const int sc = slot_tab[wi * 4 + (int)code];
+    B2_DASSERT(!(FULL || wbase + key < valid) || (sc + inword >= 0 && sc + inword < shard_n));
     if (FULL || wbase + key < valid) out[sc + inword] = IDS ? __ldcs(ids + wbase + key) : wbase + key;
   }
 }
@@ -350,11 +354,11 @@ __global__ void __launch_bounds__(kT) k_strata_scatter(const __grid_constant__ S
         __shfl_sync(0xffffffffu, next, 3) + 16 * lane - e0 - e1 - e2);  // earlier words are full
     __syncwarp();
     if (wbeg + kWarpKeys <= valid) {
-      if (ids) scatter_rounds_prefix<true, true>(word[0], tab, out, ids, wbase, wvalid);
-      else scatter_rounds_prefix<false, true>(word[0], tab, out, ids, wbase, wvalid);
+      if (ids) scatter_rounds_prefix<true, true>(word[0], tab, out, ids, wbase, wvalid, (int)(send - sbeg));
+      else scatter_rounds_prefix<false, true>(word[0], tab, out, ids, wbase, wvalid, (int)(send - sbeg));
     } else {
-      if (ids) scatter_rounds_prefix<true, false>(word[0], tab, out, ids, wbase, wvalid);
-      else scatter_rounds_prefix<false, false>(word[0], tab, out, ids, wbase, wvalid);
+      if (ids) scatter_rounds_prefix<true, false>(word[0], tab, out, ids, wbase, wvalid, (int)(send - sbeg));
+      else scatter_rounds_prefix<false, false>(word[0], tab, out, ids, wbase, wvalid, (int)(send - sbeg));
     }
     return;
   } else {
@@ -400,11 +404,11 @@ __global__ void __launch_bounds__(kT) k_strata_scatter(const __grid_constant__ S
   const int wvalid = (int)lbase + valid;
   const bool full = wbeg + kWarpKeys <= valid;
   if (full) {
-    if (ids) scatter_rounds<NB, true, true>(p, word, next, out, ids, wbase, wvalid);
-    else scatter_rounds<NB, false, true>(p, word, next, out, ids, wbase, wvalid);
+    if (ids) scatter_rounds<NB, true, true>(p, word, next, out, ids, wbase, wvalid, (int)(send - sbeg));
+    else scatter_rounds<NB, false, true>(p, word, next, out, ids, wbase, wvalid, (int)(send - sbeg));
   } else {
-    if (ids) scatter_rounds<NB, true, false>(p, word, next, out, ids, wbase, wvalid);
-    else scatter_rounds<NB, false, false>(p, word, next, out, ids, wbase, wvalid);
+    if (ids) scatter_rounds<NB, true, false>(p, word, next, out, ids, wbase, wvalid, (int)(send - sbeg));
+    else scatter_rounds<NB, false, false>(p, word, next, out, ids, wbase, wvalid, (int)(send - sbeg));
   }
   }
 }

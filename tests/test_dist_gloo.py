@@ -63,18 +63,40 @@ def _hook_worker(rank, port, q):
         dist.destroy_process_group()
 
 
-def _run(target):
+def _run(target, attempts: int = 3):
+    """WORLD gloo ranks of `target`; a rendezvous that dies early (the picked port was taken)
+    is retried on a fresh port."""
+    import queue as _queue
+    import time
+
     ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = H.free_port()
-    procs = [ctx.Process(target=target, args=(r, port, q)) for r in range(WORLD)]
-    for p in procs:
-        p.start()
-    res = dict((r, (a, b)) for r, a, b in (q.get(timeout=120) for _ in range(WORLD)))
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
-    return res
+    for attempt in range(attempts):
+        q = ctx.Queue()
+        port = H.free_port()
+        procs = [ctx.Process(target=target, args=(r, port, q)) for r in range(WORLD)]
+        for p in procs:
+            p.start()
+        res, failed, t0 = {}, False, time.monotonic()
+        while len(res) < WORLD and time.monotonic() - t0 < 120:
+            try:
+                r, a, b = q.get(timeout=2)
+                res[r] = (a, b)
+            except _queue.Empty:
+                if any(p.exitcode not in (None, 0) for p in procs):
+                    failed = True
+                    break
+        if failed and attempt + 1 < attempts:
+            for p in procs:
+                if p.is_alive():
+                    p.terminate()
+                p.join(timeout=30)
+            continue
+        assert len(res) == WORLD, f"{WORLD - len(res)} rank(s) produced no result"
+        for p in procs:
+            p.join(timeout=60)
+            assert p.exitcode == 0
+        return res
+    raise AssertionError("multi-rank run failed")
 
 
 def test_bucketwise_sync_two_ranks_matches_reference_semantics():

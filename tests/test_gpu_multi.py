@@ -107,18 +107,40 @@ def _hook_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def _run(target, world):
+def _run(target, world, attempts: int = 3):
+    """Spawn `world` ranks of `target`; a rendezvous that dies early (e.g. the picked port was
+    taken: EADDRINUSE) is retried on a fresh port instead of waiting out the queue timeout."""
+    import queue as _queue
+    import time
+
     ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = H.free_port()
-    procs = [ctx.Process(target=target, args=(r, world, port, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    res = dict(q.get(timeout=300) for _ in range(world))
-    for p in procs:
-        p.join(timeout=120)
-        assert p.exitcode == 0
-    return res
+    for attempt in range(attempts):
+        q = ctx.Queue()
+        port = H.free_port()
+        procs = [ctx.Process(target=target, args=(r, world, port, q)) for r in range(world)]
+        for p in procs:
+            p.start()
+        res, failed, t0 = {}, False, time.monotonic()
+        while len(res) < world and time.monotonic() - t0 < 300:
+            try:
+                r, v = q.get(timeout=2)
+                res[r] = v
+            except _queue.Empty:
+                if any(p.exitcode not in (None, 0) for p in procs):
+                    failed = True
+                    break
+        if failed and attempt + 1 < attempts:
+            for p in procs:
+                if p.is_alive():
+                    p.terminate()
+                p.join(timeout=30)
+            continue
+        assert len(res) == world, f"{world - len(res)} rank(s) produced no result"
+        for p in procs:
+            p.join(timeout=120)
+            assert p.exitcode == 0
+        return res
+    raise AssertionError("multi-rank run failed")
 
 
 def test_bucketwise_sync_nccl_matches_reference():
