@@ -130,9 +130,11 @@ __global__ void __launch_bounds__(RT) k_radix_upsweep(const __grid_constant__ Ra
   __shared__ uint32_t s_h[MAX_PASS][RBINS];
   __shared__ int s_unsorted;
   const int t = threadIdx.x;
-  // zero the first pass's look-back words, the tickets and the token sums
   const int64_t gt = (int64_t)blockIdx.x * RT + t, gs = (int64_t)gridDim.x * RT;
-  for (int64_t i = gt; i < p.ntiles * RBINS; i += gs) p.status[0][i] = 0u;
+  for (int64_t i = gt; i < p.ntiles * RBINS; i += gs) {
+    p.status[0][i] = 0u;
+    p.status[1][i] = 0u;
+  }
   if (p.tokens)
     for (int64_t i = gt; i < p.nseg * p.lanes; i += gs) p.tokens[i] = 0;
   if (gt < MAX_PASS) p.counters[gt] = 0u;
@@ -203,12 +205,10 @@ __global__ void __launch_bounds__(RT) k_radix_pass(const __grid_constant__ Radix
   if (t == 0) sm.tile = (int)atomicAdd(&p.counters[pass], 1u);
   __syncthreads();
   const int64_t tile = sm.tile;
-  // zero this tile's look-back words of the NEXT pass (this pass's other buffer
-  // was last used by the previous pass, which has completed in stream order)
-  if (pass + 1 < p.npass)
-    for (int d = t; d < RBINS; d += RT) p.status[(pass + 1) & 1][(size_t)tile * RBINS + d] = 0u;
   const bool unsorted = *(volatile const int32_t*)p.flags != 0;
   if (!unsorted && pass < p.npass_id) return;  // ids already ordered: length passes only
+  if (pass + 1 < p.npass)
+    for (int d = t; d < RBINS; d += RT) p.status[(pass + 1) & 1][(size_t)tile * RBINS + d] = 0u;
   const int exec = unsorted ? pass : pass - p.npass_id;  // index among the executed passes
   const bool from_input = exec == 0, last = pass == p.npass - 1;
   const int shift = p.shift[pass];
