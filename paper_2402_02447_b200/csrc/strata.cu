@@ -75,6 +75,7 @@ __device__ __forceinline__ int shard_of_tile(const StrataParams& p, int tile) {
 // last stratum and one below 1 in the first, so bad samples need no branch.
 template <int NB>
 __global__ void __launch_bounds__(kT) k_strata_count(const __grid_constant__ StrataParams p) {
+  pdl_trigger();  // the scan may launch now (it waits for this grid before reading)
   constexpr int CB = code_bits<NB>();
   constexpr int WPT = kTile * CB / 32;   // code words per tile
   constexpr int QPW = 32 / (4 * CB);     // 4-key quads per word (4 or 2)
@@ -172,6 +173,8 @@ __global__ void __launch_bounds__(kT) k_strata_count(const __grid_constant__ Str
 // the NB block scans run back to back on register sums.
 template <int NB>
 __global__ void __launch_bounds__(kScanT) k_strata_scan(const __grid_constant__ StrataParams p) {
+  pdl_trigger();
+  pdl_wait();  // the count grid's tile counts are complete and visible
   using Scan = cub::BlockScan<int, kScanT>;
   __shared__ typename Scan::TempStorage scan;
   const int g = blockIdx.x;
@@ -283,6 +286,7 @@ __device__ __forceinline__ void scatter_rounds_prefix(uint32_t word, const int* 
 
 template <int NB>
 __global__ void __launch_bounds__(kT) k_strata_scatter(const __grid_constant__ StrataParams p) {
+  pdl_wait();  // codes, tile prefixes and shard totals are complete and visible
   constexpr int CB = code_bits<NB>();
   constexpr int WPT = kTile * CB / 32;           // code words per tile
   constexpr int WPW = kWarpKeys * CB / 32;       // code words per warp (32 or 64)
@@ -422,9 +426,13 @@ static inline int64_t strata_tiles(int64_t n) { return (n + kTile - 1) / kTile; 
 
 template <int NB>
 static cudaError_t launch_all(const StrataParams& p, int64_t T, cudaStream_t st) {
+  // the scan and the scatter are programmatic dependents: their launch overlaps
+  // the previous kernel's tail, and they wait (griddepcontrol.wait) before reading
   k_strata_count<NB><<<(unsigned)T, kT, 0, st>>>(p);
-  k_strata_scan<NB><<<(unsigned)p.nshard, kScanT, 0, st>>>(p);
-  k_strata_scatter<NB><<<(unsigned)T, kT, 0, st>>>(p);
+  cudaError_t e = launch_pdl(k_strata_scan<NB>, dim3((unsigned)p.nshard), dim3(kScanT), 0, st, p);
+  if (e != cudaSuccess) return e;
+  e = launch_pdl(k_strata_scatter<NB>, dim3((unsigned)T), dim3(kT), 0, st, p);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
