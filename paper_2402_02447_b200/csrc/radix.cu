@@ -127,6 +127,7 @@ __device__ __forceinline__ void block_scan2(uint32_t a0, uint32_t a1, uint32_t b
 
 // ---------------------------------------------------------------- upsweep
 __global__ void __launch_bounds__(RT) k_radix_upsweep(const __grid_constant__ RadixParams p, int64_t tiles_per_cta) {
+  pdl_trigger();  // the first pass may launch now (it waits for this grid before reading)
   __shared__ uint32_t s_h[MAX_PASS][RBINS];
   __shared__ int s_unsorted;
   const int t = threadIdx.x;
@@ -202,6 +203,8 @@ __global__ void __launch_bounds__(RT) k_radix_pass(const __grid_constant__ Radix
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PassSmem<POS>& sm = *reinterpret_cast<PassSmem<POS>*>(smem_raw);
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  pdl_wait();     // the previous pass (or the upsweep) has completed and its writes are visible
+  pdl_trigger();  // the next pass may launch; it waits for this grid in turn
   if (t == 0) sm.tile = (int)atomicAdd(&p.counters[pass], 1u);
   __syncthreads();
   const int64_t tile = sm.tile;
@@ -538,8 +541,9 @@ extern "C" int b2_presort_sort_deal(const int32_t* ids, const int32_t* lens, int
     configured[di.device & 63][pos] = true;
   }
   for (int q = 0; q < pl.npass; ++q) {
-    if (pos) k_radix_pass<true><<<(unsigned)pl.ntiles, RT, smem, st>>>(p, q);
-    else k_radix_pass<false><<<(unsigned)pl.ntiles, RT, smem, st>>>(p, q);
+    // programmatic dependents: each pass launches under the previous kernel's tail
+    if (pos) B2_CHECK(launch_pdl(k_radix_pass<true>, dim3((unsigned)pl.ntiles), dim3(RT), smem, st, p, q));
+    else B2_CHECK(launch_pdl(k_radix_pass<false>, dim3((unsigned)pl.ntiles), dim3(RT), smem, st, p, q));
     B2_CHECK(cudaGetLastError());
   }
   return B2_OK;
