@@ -870,6 +870,53 @@ def cpu_clip_baseline(reps: int = 2) -> dict:
             "host_cpus": len(os.sched_getaffinity(0))}
 
 
+def bench_bert_base(args) -> dict:
+    """BASELINE config 0 (the reference's own CPU-runnable case): bucket-wise clip of BERT-base
+    synthetic gradients (109.5 M fp32, 17 x 25 MiB buckets), K=1: K1 in one launch (CUDA
+    events, inputs 438 MB > L2) next to the reference path on the host (same layout, same
+    per-bucket scale draw, GradientState fp64 conversion included)."""
+    import torch
+
+    import paper_2402_02447_b200 as B
+    from paper_2402_02447_b200 import synthetic
+    from oracle import ddp_oracle as O
+
+    dim = synthetic.BERT_BASE_DIM
+    g, layout, _ = synthetic.bert_grads(dim)
+    comm = torch.empty(dim, dtype=torch.bfloat16, device="cuda")
+    out32 = torch.empty(dim, dtype=torch.float32, device="cuda")
+    segs = [(a, a, b - a) for a, b in reversed(layout)]
+    clip = B.BucketClipper()
+    lim = 1.0 / math.sqrt(len(layout))
+    res = {"workload": f"BERT-base synthetic gradients (D={dim:,} fp32, {len(layout)} x 25 MiB buckets), K=1"}
+    for name, out, bpe in (("bf16_out", comm, 6), ("f32_out", out32, 8)):
+        f = clip.prepare(g, out, segs, lim)
+        for _ in range(3):
+            f()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        torch.cuda.synchronize()
+        ev[0].record()
+        for _ in range(args.steps):
+            f()
+        ev[1].record()
+        torch.cuda.synchronize()
+        us = ev[0].elapsed_time(ev[1]) / args.steps * 1e3
+        res[name] = {"us": us, "value_gbs": dim * 4 / (us * 1e-6) / 1e9, "hbm_frac": dim * bpe / (us * 1e-6) / 1e9
+                     / peaks()["hbm_gbs"]}
+    # the reference path on the host, same workload shape
+    scales = np.random.default_rng(2402).choice(np.asarray(BUCKET_SCALES), size=len(layout))
+    rng = np.random.default_rng(2402)
+    h = np.empty(dim, np.float32)
+    for (a, b), sc in zip(layout, scales):
+        h[a:b] = rng.standard_normal(b - a, dtype=np.float32) * np.float32(sc)
+    t = time.perf_counter()
+    reference_clip_step(h[None, :], layout)
+    sec = time.perf_counter() - t
+    res["cpu_baseline"] = {"value": dim * 4 / sec / 1e9, "unit": "GB/s", "cores": blas_threads(), "kind": "port",
+                           "sample": "one full step: GradientState(fp32 -> fp64) + sync_bucketwise (oracle numpy)"}
+    return res
+
+
 def cpu_presort_baseline(lens: np.ndarray, pools: dict) -> dict:
     from oracle import ddp_oracle as O
 
@@ -986,6 +1033,7 @@ def main():
     presort = None
     if rank == 0 and not args.no_presort:
         presort = bench_presort(args)
+    bert_base = bench_bert_base(args) if (world == 1 and not args.no_cpu_baseline) else None
     mc = None
     if rank == 0 and not args.no_mcsim:
         from paper_2402_02447_b200.seqdata import LengthDistribution, generate_lengths
@@ -1016,6 +1064,8 @@ def main():
                                "l2": "flushed (512 MB write) before every timed iteration", **presort}
         if mc is not None:
             line["mcsim"] = mc
+        if bert_base is not None:
+            line["config0_bert_base"] = bert_base
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_clip_baseline()
             if presort is not None:
