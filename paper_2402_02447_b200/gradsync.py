@@ -19,6 +19,7 @@ no host synchronisation).
 from __future__ import annotations
 
 import math
+import threading
 from dataclasses import dataclass
 from enum import Enum
 from typing import Any, Sequence
@@ -55,9 +56,10 @@ def capped_bucket_layout(dim: int, bucket_elems: int = BERT_BUCKET_ELEMS) -> tup
     return tuple((a, min(a + bucket_elems, dim)) for a in range(0, dim, bucket_elems))
 
 
-_STAGE_ELEMS = 8 << 20  # bytes-agnostic: elements per pinned staging slot
+_STAGE_ELEMS = 4 << 20  # elements per pinned staging slot (32 MB of fp64)
 _STAGE_SLOTS = 4
 _staging: dict = {}
+_staging_lock = threading.Lock()  # one ring per (dtype, device); callers on several threads take turns
 
 
 def _staged_h2d(src: torch.Tensor) -> torch.Tensor:
@@ -74,13 +76,19 @@ def _staged_h2d(src: torch.Tensor) -> torch.Tensor:
     if n * flat.element_size() < (64 << 20):
         out.copy_(src)
         return out
+    key = (src.dtype, torch.cuda.current_device())
+    with _staging_lock:
+        return _staged_h2d_locked(flat, out, key, src.dtype)
+
+
+def _staged_h2d_locked(flat: torch.Tensor, out: torch.Tensor, key, dtype) -> torch.Tensor:
     from concurrent.futures import ThreadPoolExecutor
 
-    key = (src.dtype, torch.cuda.current_device())
+    n = flat.numel()
     st = _staging.get(key)
     if st is None:
         st = _staging[key] = {
-            "slots": [torch.empty(_STAGE_ELEMS, dtype=src.dtype).pin_memory() for _ in range(_STAGE_SLOTS)],
+            "slots": [torch.empty(_STAGE_ELEMS, dtype=dtype).pin_memory() for _ in range(_STAGE_SLOTS)],
             "events": [None] * _STAGE_SLOTS, "stream": torch.cuda.Stream(),
             "pool": ThreadPoolExecutor(max_workers=8)}
     slots, evs, stream, pool = st["slots"], st["events"], st["stream"], st["pool"]
