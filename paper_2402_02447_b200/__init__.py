@@ -1,7 +1,8 @@
 """B200-native hot paths of arXiv 2402.02447 behind the reference ``ddpsim`` API.
 
-H1 (bucket-wise clip before allreduce): ``gradsync`` + ``ddp`` (NCCL side
-stream, DDP comm hook).  H2 (stratified local presort): ``strata`` +
+H1 (bucket-wise clip before allreduce): ``gradsync`` + ``ddp`` (fused
+NVLink kernel, NCCL side stream, DDP comm hook) + ``reducer`` (Algorithm 1 on a
+model's gradients, without DDP).  H2 (stratified local presort): ``strata`` +
 ``balance``; the Monte-Carlo balance engine in ``mcsim``.  All data passes run in ``_native/libb2ddp.so`` (sm_100a); see
 DESIGN.md.  Names mirror ``ddpsim/__init__.py:14-103`` for the in-scope paths.
 """
@@ -55,6 +56,7 @@ from .strata import (
 )
 
 from .mcsim import BalanceExperiment, BalanceStats, Strategy, run_ablation, run_balance_experiment
+from .reducer import BucketwiseReducer
 
 __version__ = "0.1.0"
 
@@ -69,4 +71,5 @@ __all__ = [
     "DeviceStrata", "Strata", "StratumAllocation", "allocate_counts", "draw_batch",
     "stratify", "stratify_lengths", "stratify_shards", "NativeDraws", "derive_seed",
     "BalanceExperiment", "BalanceStats", "Strategy", "run_ablation", "run_balance_experiment",
+    "BucketwiseReducer",
 ]
