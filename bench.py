@@ -394,13 +394,14 @@ def bench_clip(args, rank, world, local):
     host.copy_(g.view(1, -1).cpu())
     e2e_steps = max(2, min(args.steps, 5))
     if world == 1:
+        out_bf16 = torch.empty(dim, dtype=torch.bfloat16, pin_memory=True)
         out_f32 = torch.empty(dim, dtype=torch.float32, pin_memory=True)
 
         def e2e_step():  # the host-resident form of GradientState + sync_bucketwise, streamed per bucket
-            return B.sync_bucketwise_host(host, layout, cfg, out=out_f32)
-        d2h = dim * 4
-        api = ("sync_bucketwise_host (= GradientState + sync_bucketwise; pinned host fp32 in, host fp32 out; "
-               "H2D / K1 / D2H streamed per bucket)")
+            return B.sync_bucketwise_host(host, layout, cfg, out=out_bf16)
+        d2h = dim * 2
+        api = ("sync_bucketwise_host (= GradientState + sync_bucketwise; pinned host fp32 in, host bf16 out — "
+               "the step's comm dtype, as at N>1; H2D / K1 / D2H streamed per bucket)")
     else:
         out_host = torch.empty(dim, dtype=torch.bfloat16, pin_memory=True)
         if launches_per_step == 1:
@@ -427,6 +428,13 @@ def bench_clip(args, rank, world, local):
     e2e_s = max_over_ranks(time.perf_counter() - ts, world) / e2e_steps
     res["e2e"] = {"value": world * dim * 4 / e2e_s / 1e9, "unit": "GB/s", "ms_per_step": e2e_s * 1e3,
                   "h2d_bytes_per_step": dim * 4, "d2h_bytes_per_step": d2h, "steps": e2e_steps, "api": api}
+    if world == 1:  # the same call returning the fp32 result (2 x 1.34 GB over PCIe)
+        B.sync_bucketwise_host(host, layout, cfg, out=out_f32)
+        ts = time.perf_counter()
+        for _ in range(e2e_steps):
+            B.sync_bucketwise_host(host, layout, cfg, out=out_f32)
+        t32 = (time.perf_counter() - ts) / e2e_steps
+        res["e2e"]["f32_out"] = {"value": dim * 4 / t32 / 1e9, "ms_per_step": t32 * 1e3, "d2h_bytes_per_step": dim * 4}
     del host
     if world == 1:
         # the drop-in call exactly as a reference user makes it: a host fp64 (1, D) numpy array

@@ -443,9 +443,12 @@ def sync_bucketwise_host(workers, bucket_layout, cfg: ClipConfig, out: torch.Ten
     b — so both PCIe directions run at once instead of one after the other.
     A non-finite input raises ``ValueError`` ("gradient state has non-finite
     components") before any result is returned.  ``out`` may be a pinned
-    host tensor to receive the result (else a pinned one is allocated); the
-    host input should be pinned for full PCIe rate.  Single worker (K = 1);
-    K > 1 goes through GradientState + sync_bucketwise.
+    host tensor to receive the result (else a pinned one is allocated): of
+    the input's dtype (the result comes back as numpy), or bfloat16 — the
+    comm-buffer dtype of the multi-rank step — which halves the device->host
+    bytes and comes back as that torch tensor.  The host input should be
+    pinned for full PCIe rate.  Single worker (K = 1); K > 1 goes through
+    GradientState + sync_bucketwise.
     """
     _require_mode(cfg, ClipMode.BUCKET_WISE)
     src = workers if isinstance(workers, torch.Tensor) else torch.from_numpy(
@@ -467,11 +470,11 @@ def sync_bucketwise_host(workers, bucket_layout, cfg: ClipConfig, out: torch.Ten
     compute = torch.cuda.current_stream(dev)
     h2d, d2h = _host_streams(dev)
     d_in = torch.empty(D, dtype=g.dtype, device=dev)
-    d_out = torch.empty(D, dtype=g.dtype, device=dev)
     if out is None:
         out = torch.empty(D, dtype=g.dtype, pin_memory=True)
-    elif out.numel() != D or out.dtype != g.dtype:
-        raise ValueError(f"out must be a host {g.dtype} tensor of {D} elements")
+    elif out.numel() != D or out.dtype not in (g.dtype, torch.bfloat16) or out.is_cuda:
+        raise ValueError(f"out must be a host {g.dtype} or bfloat16 tensor of {D} elements")
+    d_out = torch.empty(D, dtype=out.dtype, device=dev)
     flags = torch.empty(len(layout), dtype=torch.int32, device=dev)
     c = _clipper()
     h2d.wait_stream(compute)  # d_in / d_out are fresh allocations of the compute stream
@@ -492,7 +495,7 @@ def sync_bucketwise_host(workers, bucket_layout, cfg: ClipConfig, out: torch.Ten
     d_out.record_stream(d2h)
     if bool(flags.any()):  # synchronises: every copy has landed
         raise ValueError("gradient state has non-finite components")
-    return out.numpy()
+    return out if out.dtype == torch.bfloat16 else out.numpy()
 
 
 _host_stream_cache: dict = {}

@@ -417,3 +417,21 @@ def test_gradient_state_staged_host_copy_is_exact():
     w32 = w[0].astype(np.float32)[None, :]
     st32 = GradientState(torch.from_numpy(w32), equal_bucket_layout(w.shape[1], 5))  # fp32 tensor stays fp32
     assert st32.workers.dtype == torch.float32 and np.array_equal(st32.workers.cpu().numpy(), w32)
+
+
+def test_sync_bucketwise_host_bf16_out():
+    """The host-resident step returning the bf16 comm-dtype result (half the D2H bytes):
+    within one bf16 rounding of the reference's sync_bucketwise, as a torch tensor."""
+    rng = np.random.default_rng(21)
+    w = (rng.standard_normal((1, 3_000_017)) * rng.choice([1e-4, 1e-2], size=(1, 3_000_017))).astype(np.float32)
+    layout = equal_bucket_layout(w.shape[1], 7)
+    host = torch.from_numpy(w).pin_memory()
+    out = torch.empty(w.shape[1], dtype=torch.bfloat16).pin_memory()
+    from paper_2402_02447_b200 import sync_bucketwise_host
+
+    got = sync_bucketwise_host(host, layout, BUCKET, out=out)
+    assert got is out and got.dtype == torch.bfloat16
+    ref = O.sync_bucketwise(w.astype(np.float64), layout, 1.0)
+    assert rel_err(got.float().numpy(), ref) <= 2.0 ** -8
+    with pytest.raises(ValueError, match="bfloat16"):
+        sync_bucketwise_host(host, layout, BUCKET, out=torch.empty(w.shape[1], dtype=torch.float16))
