@@ -91,8 +91,14 @@ def test_train_step_modes_small_bert(mode):
     small = dict(vocab_size=1024, hidden_size=128, num_hidden_layers=2, num_attention_heads=2,
                  intermediate_size=256, max_position_embeddings=128)
     lens = generate_lengths(LengthDistribution(), 50_000, 3)
-    r = bert_large_step_bench(mode, steps=2, warmup=2, batch=8, seq=128, bucket_cap_mb=1, lengths=lens,
-                              model_config=small)
+    import torch.distributed as dist
+
+    try:
+        r = bert_large_step_bench(mode, steps=2, warmup=2, batch=8, seq=128, bucket_cap_mb=1, lengths=lens,
+                                  model_config=small)
+    finally:
+        if dist.is_initialized():  # the step bench initialised a world-size-1 NCCL group
+            dist.destroy_process_group()
     assert np.isfinite(r["loss"]) and r["samples_per_s"] > 0
     if mode == "bucketwise":
         assert r["buckets_iter0"]["predicted"] == r["buckets_iter0"]["ddp"]
