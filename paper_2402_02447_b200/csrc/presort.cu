@@ -221,7 +221,8 @@ __global__ void __launch_bounds__(32 * kCntWarps, MINB) k_presort_deal_count(con
   __syncwarp();
   for (int64_t seg = (int64_t)blockIdx.x * kCntWarps + w; seg < p.nseg; seg += nwarps) {
     const int64_t base = seg * P;
-    if (seg + nwarps < p.nseg) {  // next pool of this warp -> L2
+    if (KM > 4 && seg + nwarps < p.nseg) {  // next pool of this warp -> L2 (128-key pools: other warps hide the
+      // loads and the prefetch only costs instructions, 75.8 -> 69.6 us at lb16)
       const int64_t nb = base + nwarps * P;
       const int nl = (P * 4 + 127) / 128 + 1;
       for (int k = lane; k < 2 * nl; k += 32) {
