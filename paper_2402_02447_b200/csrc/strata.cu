@@ -48,6 +48,7 @@ struct StrataParams {
   const int32_t* ids;  // may be null: id = index within the shard
   int nb, nshard;
   int32_t bounds[kMaxStrata];
+  int shift;  // >= 0: bounds are (q+1) << shift (the count pass shifts instead of comparing)
   int64_t shard_off[kMaxShards + 1];  // element offset of each shard
   int32_t tile_off[kMaxShards + 1];   // first tile of each shard
   int32_t* tile_counts;               // [T][kMaxStrata]: counts, then exclusive in-shard prefixes
@@ -73,7 +74,7 @@ __device__ __forceinline__ int shard_of_tile(const StrataParams& p, int tile) {
 // pass 1: codes + per-tile counts (+ the shard's first bad sample).  The code is
 // sum_{q < nb-1} (len > bound_q): a length above the last bound lands in the
 // last stratum and one below 1 in the first, so bad samples need no branch.
-template <int NB>
+template <int NB, bool UNIFORM>
 __global__ void __launch_bounds__(kT) k_strata_count(const __grid_constant__ StrataParams p) {
   pdl_trigger();  // the scan may launch now (it waits for this grid before reading)
   constexpr int CB = code_bits<NB>();
@@ -120,8 +121,13 @@ __global__ void __launch_bounds__(kT) k_strata_count(const __grid_constant__ Str
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       int k = 0;
+      if constexpr (UNIFORM) {
+        // bounds (q+1) * 2^shift: searchsorted(..., 'left') = (len-1) >> shift, clamped
+        k = min(max((x[e] - 1) >> p.shift, 0), p.nb - 1);
+      } else {
 #pragma unroll
-      for (int q = 0; q < NB - 1; ++q) k += (x[e] > bnd[q]);  // == searchsorted(..., 'left')
+        for (int q = 0; q < NB - 1; ++q) k += (x[e] > bnd[q]);  // == searchsorted(..., 'left')
+      }
       anybad |= (uint32_t)(x[e] - 1) >= blast;               // len < 1 or len > last bound
       packed |= (uint32_t)k << (e * CB);
     }
@@ -428,7 +434,8 @@ template <int NB>
 static cudaError_t launch_all(const StrataParams& p, int64_t T, cudaStream_t st) {
   // the scan and the scatter are programmatic dependents: their launch overlaps
   // the previous kernel's tail, and they wait (griddepcontrol.wait) before reading
-  k_strata_count<NB><<<(unsigned)T, kT, 0, st>>>(p);
+  if (p.shift >= 0) k_strata_count<NB, true><<<(unsigned)T, kT, 0, st>>>(p);
+  else k_strata_count<NB, false><<<(unsigned)T, kT, 0, st>>>(p);
   cudaError_t e = launch_pdl(k_strata_scan<NB>, dim3((unsigned)p.nshard), dim3(kScanT), 0, st, p);
   if (e != cudaSuccess) return e;
   e = launch_pdl(k_strata_scatter<NB>, dim3((unsigned)T), dim3(kT), 0, st, p);
@@ -462,6 +469,12 @@ extern "C" int b2_strata_partition_shards(const int32_t* lengths, const int32_t*
   p.nb = nb;
   p.nshard = nshard;
   for (int k = 0; k < kMaxStrata; ++k) p.bounds[k] = k < nb ? bounds[k] : INT32_MAX;
+  p.shift = -1;  // uniform power-of-two strata (e.g. the default 128/256/384/512)?
+  for (int sh = 0; sh < 31 && p.shift < 0; ++sh) {
+    bool ok = true;
+    for (int k = 0; k < nb && ok; ++k) ok = (int64_t)bounds[k] == ((int64_t)(k + 1) << sh);
+    if (ok) p.shift = sh;
+  }
   int64_t T = 0;
   p.shard_off[0] = shard_off[0];
   for (int g = 0; g < nshard; ++g) {
