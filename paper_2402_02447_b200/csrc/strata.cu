@@ -301,24 +301,28 @@ __global__ void __launch_bounds__(kT) k_strata_scatter(const __grid_constant__ S
   __shared__ int s_wcnt[kT / 32][kMaxStrata];
   __shared__ int s_dst[kMaxStrata];
   __shared__ __align__(16) int s_slot[kT / 32][CB == 2 ? 32 * 4 : 1];  // [word][code] first slots (<= 4 strata)
+  __shared__ int s_g;
   const int tile = blockIdx.x;
-  const int g = shard_of_tile(p, tile);
-  const int64_t sbeg = p.shard_off[g], send = p.shard_off[g + 1];
-  const int64_t lbase = (int64_t)(tile - p.tile_off[g]) * kTile;
-  const int valid = (int)min64(kTile, send - sbeg - lbase);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (threadIdx.x == 0) {  // this tile's first slot per stratum (in-shard): earlier strata + earlier tiles
-    int gb = 0;
-    for (int k = 0; k < p.nb; ++k) {
-      s_dst[k] = gb + p.tile_counts[(int64_t)tile * kMaxStrata + k];
-      gb += (int)p.counts[(int64_t)g * p.nb + k];
-    }
-  }
   const int wbeg = w * kWarpKeys;  // first key of this warp in the tile
   uint32_t word[WPL];
   const uint32_t* cw = p.codes + (int64_t)tile * WPT + w * WPW;
 #pragma unroll
-  for (int i = 0; i < WPL; ++i) word[i] = __ldcs(cw + lane * WPL + i);
+  for (int i = 0; i < WPL; ++i) word[i] = __ldcs(cw + lane * WPL + i);  // in flight during the lookup below
+  if (threadIdx.x == 0) {  // the tile's shard (one lookup per CTA) and its first slot per stratum (in-shard):
+    const int g0 = shard_of_tile(p, tile);  // earlier strata + earlier tiles
+    s_g = g0;
+    int gb = 0;
+    for (int k = 0; k < p.nb; ++k) {
+      s_dst[k] = gb + p.tile_counts[(int64_t)tile * kMaxStrata + k];
+      gb += (int)p.counts[(int64_t)g0 * p.nb + k];
+    }
+  }
+  __syncthreads();
+  const int g = s_g;
+  const int64_t sbeg = p.shard_off[g], send = p.shard_off[g + 1];
+  const int64_t lbase = (int64_t)(tile - p.tile_off[g]) * kTile;
+  const int valid = (int)min64(kTile, send - sbeg - lbase);
   if constexpr (CB == 2) {
     // per-word counts of codes 0..2 (keys beyond `valid` masked out), packed 10 bits each
     constexpr uint32_t LOW = 0x55555555u;
@@ -347,7 +351,9 @@ __global__ void __launch_bounds__(kT) k_strata_scatter(const __grid_constant__ S
     int next = 0;  // lane k < nb: first slot of stratum k for this warp (within the shard)
     if (lane < p.nb) {
       int off = s_dst[lane];
-      for (int u = 0; u < w; ++u) off += s_wcnt[u][lane];
+#pragma unroll
+      for (int u = 0; u < kT / 32 - 1; ++u)
+        if (u < w) off += s_wcnt[u][lane];
       next = off;
     }
     int32_t* out = p.ids_out + sbeg;
@@ -405,7 +411,9 @@ __global__ void __launch_bounds__(kT) k_strata_scatter(const __grid_constant__ S
   int next = 0;  // lane k < nb: next output slot of stratum k for this warp (within the shard)
   if (lane < p.nb) {
     int off = s_dst[lane];
-    for (int u = 0; u < w; ++u) off += s_wcnt[u][lane];
+#pragma unroll
+    for (int u = 0; u < kT / 32 - 1; ++u)
+      if (u < w) off += s_wcnt[u][lane];
     next = off;
   }
   int32_t* out = p.ids_out + sbeg;
