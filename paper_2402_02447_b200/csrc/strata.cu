@@ -51,7 +51,7 @@ struct StrataParams {
   int shift;  // >= 0: bounds are (q+1) << shift (the count pass shifts instead of comparing)
   int64_t shard_off[kMaxShards + 1];  // element offset of each shard
   int32_t tile_off[kMaxShards + 1];   // first tile of each shard
-  int32_t* tile_counts;               // [T][kMaxStrata]: counts, then exclusive in-shard prefixes
+  int32_t* tile_counts;               // [T][kMaxStrata]: counts, then the tile's first in-shard slot per stratum
   uint32_t* codes;                    // [T][kTile * CB / 32] packed stratum codes
   int64_t* counts;                    // [nshard][nb] totals
   int64_t* bad;                       // [nshard] first bad index within the shard (u64 min), pre-set to -1
@@ -173,8 +173,9 @@ __global__ void __launch_bounds__(kT) k_strata_count(const __grid_constant__ Str
   if (threadIdx.x < NB) p.tile_counts[(int64_t)tile * kMaxStrata + threadIdx.x] = threadIdx.x < p.nb ? cnt[threadIdx.x] : 0;
 }
 
-// pass 1b: one CTA per shard turns its tile counts into exclusive in-shard
-// prefixes (in place) and writes the shard totals.  Each thread owns a run
+// pass 1b: one CTA per shard turns its tile counts into each tile's first
+// in-shard slot per stratum (exclusive prefix + the earlier strata's totals,
+// in place) and writes the shard totals.  Each thread owns a run
 // of consecutive tiles and reads each tile's count row once (16 B vectors);
 // the NB block scans run back to back on register sums.
 template <int NB>
@@ -199,12 +200,15 @@ __global__ void __launch_bounds__(kScanT) k_strata_scan(const __grid_constant__ 
     }
   }
   int ex[NB];
+  int base = 0;  // slots of the earlier strata in this shard: the prefixes are final in-shard slots
 #pragma unroll
   for (int k = 0; k < NB; ++k) {
     int agg;
     if (k) __syncthreads();  // scan storage reuse
     Scan(scan).ExclusiveSum(sum[k], ex[k], agg);
     if (threadIdx.x == 0 && k < p.nb) p.counts[(int64_t)g * p.nb + k] = agg;
+    ex[k] += base;
+    base += agg;
   }
   for (int t = a; t < b; ++t) {
     int4* row = reinterpret_cast<int4*>(p.tile_counts + (int64_t)t * kMaxStrata);
@@ -309,15 +313,8 @@ __global__ void __launch_bounds__(kT) k_strata_scatter(const __grid_constant__ S
   const uint32_t* cw = p.codes + (int64_t)tile * WPT + w * WPW;
 #pragma unroll
   for (int i = 0; i < WPL; ++i) word[i] = __ldcs(cw + lane * WPL + i);  // in flight during the lookup below
-  if (threadIdx.x == 0) {  // the tile's shard (one lookup per CTA) and its first slot per stratum (in-shard):
-    const int g0 = shard_of_tile(p, tile);  // earlier strata + earlier tiles
-    s_g = g0;
-    int gb = 0;
-    for (int k = 0; k < p.nb; ++k) {
-      s_dst[k] = gb + p.tile_counts[(int64_t)tile * kMaxStrata + k];
-      gb += (int)p.counts[(int64_t)g0 * p.nb + k];
-    }
-  }
+  if (threadIdx.x < NB) s_dst[threadIdx.x] = p.tile_counts[(int64_t)tile * kMaxStrata + threadIdx.x];  // first in-shard slot per stratum
+  if (threadIdx.x == 0) s_g = shard_of_tile(p, tile);  // the tile's shard: one lookup per CTA
   __syncthreads();
   const int g = s_g;
   const int64_t sbeg = p.shard_off[g], send = p.shard_off[g + 1];
