@@ -25,7 +25,7 @@
 //                     id is stored straight to its final slot (a round writes
 //                     <= nb contiguous runs: coalesced, no staging).
 // A bad sample (length < 1 or above the last bound) is reported through
-// `bad` (the wrapper raises like the reference); it is placed in the nearest
+// `bad` (the wrapper raises like the reference); it is placed in an edge
 // stratum, so ids_out/counts of that shard are unspecified.
 #include "common.cuh"
 
@@ -73,7 +73,8 @@ __device__ __forceinline__ int shard_of_tile(const StrataParams& p, int tile) {
 
 // pass 1: codes + per-tile counts (+ the shard's first bad sample).  The code is
 // sum_{q < nb-1} (len > bound_q): a length above the last bound lands in the
-// last stratum and one below 1 in the first, so bad samples need no branch.
+// last stratum and one below 1 in the first (the last with shift codes), so
+// bad samples need no branch.
 template <int NB, bool UNIFORM>
 __global__ void __launch_bounds__(kT) k_strata_count(const __grid_constant__ StrataParams p) {
   pdl_trigger();  // the scan may launch now (it waits for this grid before reading)
@@ -122,8 +123,9 @@ __global__ void __launch_bounds__(kT) k_strata_count(const __grid_constant__ Str
     for (int e = 0; e < 4; ++e) {
       int k = 0;
       if constexpr (UNIFORM) {
-        // bounds (q+1) * 2^shift: searchsorted(..., 'left') = (len-1) >> shift, clamped
-        k = min(max((x[e] - 1) >> p.shift, 0), p.nb - 1);
+        // bounds (q+1) * 2^shift: searchsorted(..., 'left') = (len-1) >> shift, clamped (a
+        // length below 1 wraps to the last stratum: bad, the shard's output is unspecified)
+        k = (int)min((uint32_t)(x[e] - 1) >> p.shift, (uint32_t)(p.nb - 1));
       } else {
 #pragma unroll
         for (int q = 0; q < NB - 1; ++q) k += (x[e] > bnd[q]);  // == searchsorted(..., 'left')
@@ -164,9 +166,7 @@ __global__ void __launch_bounds__(kT) k_strata_count(const __grid_constant__ Str
   }
 #pragma unroll
   for (int q = 0; q < NB; ++q) {
-    int v = c[q];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int v = (int)__reduce_add_sync(0xffffffffu, (unsigned)c[q]);  // one REDUX per stratum
     if (lane == 0 && v && q < p.nb) atomicAdd(&cnt[q], v);
   }
   __syncthreads();
