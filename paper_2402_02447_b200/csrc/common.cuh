@@ -63,6 +63,15 @@ inline int check_cuda(cudaError_t e, const char* what) {
   } while (0)
 #endif
 
+// A pointer the compiler may not re-associate with later index arithmetic: keeps
+// `base + (uint32_t)i` a single IMAD.WIDE.U32 instead of a 64-bit add + shifts.
+template <typename T>
+__device__ __forceinline__ T* opaque(T* p) {
+  asm("mov.b64 %0, %0;" : "+l"(p));
+  __builtin_assume(__isGlobal(p));  // still a global pointer: STG, not generic ST
+  return p;
+}
+
 // ---- programmatic dependent launch ----------------------------------------
 // A kernel launched with launch_pdl() may start while its predecessor in the
 // stream drains; it must call pdl_wait() before touching anything the

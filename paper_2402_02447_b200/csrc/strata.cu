@@ -290,7 +290,9 @@ __device__ __forceinline__ void scatter_rounds_prefix(uint32_t word, const int* 
     const int inword = __popc(~(y | (y >> 1)) & below);
     const int sc = slot_tab[wi * 4 + (int)code];
     B2_DASSERT(!(FULL || wbase + key < valid) || (sc + inword >= 0 && sc + inword < shard_n));
-    if (FULL || wbase + key < valid) out[sc + inword] = IDS ? __ldcs(ids + wbase + key) : wbase + key;
+    // unsigned in-shard slot: one IMAD.WIDE.U32 per address instead of a 64-bit add + shifts
+    if (FULL || wbase + key < valid)
+      out[(uint32_t)(sc + inword)] = IDS ? __ldcs(ids + (uint32_t)(wbase + key)) : wbase + key;
   }
 }
 
@@ -353,7 +355,7 @@ __global__ void __launch_bounds__(kT) k_strata_scatter(const __grid_constant__ S
         if (u < w) off += s_wcnt[u][lane];
       next = off;
     }
-    int32_t* out = p.ids_out + sbeg;
+    int32_t* out = opaque(p.ids_out + sbeg);  // one base register: slot addresses are one IMAD.WIDE.U32
     const int wbase = (int)lbase + wbeg;  // shard-local index of this warp's first key
     const int32_t* ids = p.ids ? p.ids + sbeg : nullptr;
     const int wvalid = (int)lbase + valid;
@@ -399,9 +401,7 @@ __global__ void __launch_bounds__(kT) k_strata_scatter(const __grid_constant__ S
   }
 #pragma unroll
   for (int k = 0; k < NB; ++k) {
-    int v = mine[k];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int v = (int)__reduce_add_sync(0xffffffffu, (unsigned)mine[k]);
     if (lane == k) s_wcnt[w][k] = v;
   }
   __syncthreads();
