@@ -15,24 +15,29 @@
 // like Timsort, and each sample's input slot can ride along (out_pos).
 //
 // Launches (per call, every segment at once):
-//   k_radix_upsweep : one read of (id, len): validates, counts every pass's
-//                     digit histogram per segment (shared-memory histograms,
-//                     flushed once per run of tiles), detects whether ids are
-//                     already non-decreasing inside every segment, and zeroes
-//                     the first pass's look-back state and the token sums.
-//   k_radix_pass x P: onesweep — one read + one write per key per pass.  A
-//                     tile (4096 keys, never straddling segments) ranks its
-//                     keys stably (warp match_any + per-warp digit counters),
-//                     publishes per-digit counts and resolves its global
-//                     per-digit offsets by decoupled look-back over the
-//                     preceding tiles of its segment (tile order = atomic
-//                     ticket order, so a predecessor is always running or
+//   k_radix_hist<false> (upsweep): one read of (id, len), kept in L2: validates,
+//                     counts the length digits' histograms per segment
+//                     (shared-memory histograms, flushed once per run of
+//                     tiles), detects whether ids are already non-decreasing
+//                     inside every segment, zeroes the look-back state and
+//                     the token sums.
+//   k_radix_hist<true>: the id digits' histograms; returns at once when the
+//                     ids are already ordered.
+//   k_radix_pass x P: onesweep -- one read + one write per key per pass.  A
+//                     persistent grid takes tiles (4096 keys, never
+//                     straddling segments) by atomic ticket, round-robin over
+//                     the segments.  A tile ranks its keys stably (per-bit
+//                     warp ballots give each key's peer group; the group's
+//                     leader takes its slots from the warp's digit counter
+//                     with one shared atomic), publishes per-digit counts
+//                     and resolves its global per-digit offsets by decoupled
+//                     look-back over the preceding tiles of its segment
+//                     (ticket order, so a predecessor is always running or
 //                     done), stages the tile digit-sorted in shared memory
 //                     and writes runs with consecutive addresses.  The last
 //                     pass writes the deal directly: sorted slot q of a
 //                     segment -> row q / lanes, lane (snake-reversed on odd
-//                     rows) -> out_ids[seg][lane][row]; token sums are
-//                     accumulated per tile in shared memory.
+//                     rows) -> out_ids[seg][lane][row]; token sums per lane.
 // If the upsweep finds ids non-decreasing inside every segment (a rank shard
 // in id order, the stratified shard of K2, ...) the id-digit passes are
 // skipped on the device (no host round trip): a stable sort by length alone
@@ -90,6 +95,21 @@ __device__ __forceinline__ void st_relaxed_u32(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// 4 B load that asks L2 to keep the line (evict_last): the upsweep's reads of
+// (id, len) stay resident for the first pass, which reads them again
+__device__ __forceinline__ int32_t ld_keep(const int32_t* a, uint64_t pol) {
+  int32_t v;
+  asm volatile("ld.global.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* a) { asm volatile("prefetch.global.L2 [%0];" ::"l"(a)); }
+
 __device__ __forceinline__ unsigned long long make_key(const RadixParams& p, int32_t L, int32_t D) {
   L = L < 1 ? 1 : (L > p.max_len ? p.max_len : L);  // out-of-range samples are reported via bad
   D = D < 0 ? 0 : (D > p.max_id ? p.max_id : D);
@@ -126,22 +146,51 @@ __device__ __forceinline__ void block_scan2(uint32_t a0, uint32_t a1, uint32_t b
 }
 
 // ---------------------------------------------------------------- upsweep
-__global__ void __launch_bounds__(RT) k_radix_upsweep(const __grid_constant__ RadixParams p, int64_t tiles_per_cta) {
-  pdl_trigger();  // the first pass may launch now (it waits for this grid before reading)
+// Two histogram launches, UKEYS (len, id) loads in flight per thread per tile
+// round (no barrier inside a round, so they issue back to back):
+//   k_radix_hist<false> (the upsweep proper): validates, detects whether ids
+//     are non-decreasing inside every segment, zeroes the look-back state and
+//     the token sums, and builds the LENGTH digits' histograms;
+//   k_radix_hist<true>: the id digits' histograms -- only needed when some
+//     segment's ids decrease, so an ordered shard (the stratified rank shard)
+//     returns at once and never pays for them.
+constexpr int UKEYS = 16;
+static_assert(UKEYS * RT == TILE, "one upsweep round covers a tile");
+template <bool IDS>
+__global__ void __launch_bounds__(RT, 4) k_radix_hist(const __grid_constant__ RadixParams p, int64_t tiles_per_cta) {
   __shared__ uint32_t s_h[MAX_PASS][RBINS];
   __shared__ int s_unsorted;
-  const int t = threadIdx.x;
-  const int64_t gt = (int64_t)blockIdx.x * RT + t, gs = (int64_t)gridDim.x * RT;
-  for (int64_t i = gt; i < p.ntiles * RBINS; i += gs) {
-    p.status[0][i] = 0u;
-    p.status[1][i] = 0u;
+  const int t = threadIdx.x, lane = t & 31;
+  if constexpr (IDS) {
+    pdl_wait();  // the upsweep's sortedness flag
+    pdl_trigger();
+    if (*(volatile const int32_t*)p.flags == 0) return;
+  } else {
+    pdl_trigger();  // the next launch may start; it waits for this grid before reading
   }
-  if (p.tokens)
-    for (int64_t i = gt; i < p.nseg * p.lanes; i += gs) p.tokens[i] = 0;
-  if (gt < MAX_PASS) p.counters[gt] = 0u;
-  if (t == 0) s_unsorted = 0;
-  for (int i = t; i < p.npass * RBINS; i += RT) (&s_h[0][0])[i] = 0u;
+  const int q0 = IDS ? 0 : p.npass_id, q1 = IDS ? p.npass_id : p.npass;  // digits counted here
+  const int64_t gt = (int64_t)blockIdx.x * RT + t, gs = (int64_t)gridDim.x * RT;
+  if constexpr (!IDS) {
+    for (int64_t i = gt; i < p.ntiles * RBINS; i += gs) {
+      p.status[0][i] = 0u;
+      p.status[1][i] = 0u;
+    }
+    if (p.tokens)
+      for (int64_t i = gt; i < p.nseg * p.lanes; i += gs) p.tokens[i] = 0;
+    if (gt < MAX_PASS) p.counters[gt] = 0u;
+    if (t == 0) s_unsorted = 0;
+  }
+  for (int i = t; i < MAX_PASS * RBINS; i += RT) (&s_h[0][0])[i] = 0u;
   __syncthreads();
+  auto flush = [&](int64_t seg) {
+    for (int i = q0 * RBINS + t; i < q1 * RBINS; i += RT) {
+      const uint32_t c = (&s_h[0][0])[i];
+      if (c) {
+        atomicAdd(&p.hist[((size_t)(i / RBINS) * p.nseg + seg) * RBINS + (i % RBINS)], c);
+        (&s_h[0][0])[i] = 0u;
+      }
+    }
+  };
   const int64_t tile0 = (int64_t)blockIdx.x * tiles_per_cta;
   const int64_t tile1 = min64(tile0 + tiles_per_cta, p.ntiles);
   int64_t cur_seg = tile0 < tile1 ? tile0 / p.tps : -1;
@@ -151,38 +200,57 @@ __global__ void __launch_bounds__(RT) k_radix_upsweep(const __grid_constant__ Ra
     const int64_t seg = tile / p.tps;
     if (seg != cur_seg) {  // flush the finished segment's histograms
       __syncthreads();
-      for (int i = t; i < p.npass * RBINS; i += RT) {
-        const uint32_t c = (&s_h[0][0])[i];
-        if (c) {
-          atomicAdd(&p.hist[((size_t)(i / RBINS) * p.nseg + cur_seg) * RBINS + (i % RBINS)], c);
-          (&s_h[0][0])[i] = 0u;
-        }
-      }
+      flush(cur_seg);
       __syncthreads();
       cur_seg = seg;
     }
     const int64_t sbase = seg * (int64_t)p.seg_len;
     const int in0 = (int)(tile - seg * p.tps) * TILE;
     const int n = min(TILE, p.seg_len - in0);
-    for (int i = t; i < n; i += RT) {  // striped: coalesced
-      const int64_t g = sbase + in0 + i;
-      const int32_t L = p.lens[g], D = p.ids[g];
-      if (!(L >= 1 && L <= p.max_len && D >= 0 && D <= p.max_id) && first_bad < 0) first_bad = g;
-      if (in0 + i + 1 < p.seg_len && p.ids[g + 1] < D) unsorted = 1;  // neighbour: an L1/L2 hit
-      const unsigned long long k = make_key(p, L, D);
-      for (int q = 0; q < p.npass; ++q)
-        atomicAdd(&s_h[q][(uint32_t)(k >> p.shift[q]) & ((1u << p.bits[q]) - 1u)], 1u);
+    int32_t L[UKEYS], D[UKEYS];
+    const uint64_t pol = policy_evict_last();
+#pragma unroll
+    for (int j = 0; j < UKEYS; ++j) {  // striped: coalesced, all loads in flight
+      const int i = j * RT + t;
+      L[j] = 1;
+      D[j] = 0;
+      if (i < n) {
+        if constexpr (IDS) {
+          D[j] = __ldg(p.ids + sbase + in0 + i);
+        } else {
+          D[j] = ld_keep(p.ids + sbase + in0 + i, pol);
+          L[j] = ld_keep(p.lens + sbase + in0 + i, pol);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < UKEYS; ++j) {
+      const int i = j * RT + t;
+      const bool valid = i < n;
+      if constexpr (!IDS) {
+        const int64_t g = sbase + in0 + i;
+        // the next key's id: lane+1's, or (lane 31 / the tile's last key) one load that hits L1/L2
+        int32_t nxt = __shfl_down_sync(0xffffffffu, D[j], 1);
+        if (valid && (lane == 31 || i + 1 >= n)) nxt = in0 + i + 1 < p.seg_len ? __ldg(p.ids + g + 1) : 0x7fffffff;
+        if (valid) {
+          if (!(L[j] >= 1 && L[j] <= p.max_len && D[j] >= 0 && D[j] <= p.max_id) && first_bad < 0) first_bad = g;
+          if (nxt < D[j]) unsorted = 1;
+        }
+      }
+      if (valid) {
+        const unsigned long long k = make_key(p, L[j], D[j]);
+        for (int q = q0; q < q1; ++q) atomicAdd(&s_h[q][(uint32_t)(k >> p.shift[q]) & ((1u << p.bits[q]) - 1u)], 1u);
+      }
     }
   }
-  if (unsorted) s_unsorted = 1;
-  if (first_bad >= 0 && p.bad) atomicMin(reinterpret_cast<unsigned long long*>(p.bad), (unsigned long long)first_bad);
+  if constexpr (!IDS) {
+    if (unsorted) s_unsorted = 1;
+    if (first_bad >= 0 && p.bad) atomicMin(reinterpret_cast<unsigned long long*>(p.bad), (unsigned long long)first_bad);
+  }
   __syncthreads();
-  if (cur_seg >= 0)
-    for (int i = t; i < p.npass * RBINS; i += RT) {
-      const uint32_t c = (&s_h[0][0])[i];
-      if (c) atomicAdd(&p.hist[((size_t)(i / RBINS) * p.nseg + cur_seg) * RBINS + (i % RBINS)], c);
-    }
-  if (t == 0 && s_unsorted) atomicOr(p.flags, 1);
+  if (cur_seg >= 0) flush(cur_seg);
+  if constexpr (!IDS)
+    if (t == 0 && s_unsorted) atomicOr(p.flags, 1);
 }
 
 // ---------------------------------------------------------------- onesweep pass
@@ -199,25 +267,23 @@ struct PassSmem {
 };
 
 template <bool POS>
-__global__ void __launch_bounds__(RT) k_radix_pass(const __grid_constant__ RadixParams p, int pass) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  PassSmem<POS>& sm = *reinterpret_cast<PassSmem<POS>*>(smem_raw);
+__device__ __forceinline__ void radix_tile(const RadixParams& p, int pass, bool unsorted, int64_t ticket,
+                                           PassSmem<POS>& sm) {
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  pdl_wait();     // the previous pass (or the upsweep) has completed and its writes are visible
-  pdl_trigger();  // the next pass may launch; it waits for this grid in turn
-  if (t == 0) sm.tile = (int)atomicAdd(&p.counters[pass], 1u);
-  __syncthreads();
-  const int64_t tile = sm.tile;
-  const bool unsorted = *(volatile const int32_t*)p.flags != 0;
-  if (!unsorted && pass < p.npass_id) return;  // ids already ordered: length passes only
-  if (pass + 1 < p.npass)
-    for (int d = t; d < RBINS; d += RT) p.status[(pass + 1) & 1][(size_t)tile * RBINS + d] = 0u;
   const int exec = unsorted ? pass : pass - p.npass_id;  // index among the executed passes
   const bool from_input = exec == 0, last = pass == p.npass - 1;
   const int shift = p.shift[pass];
-  const uint32_t mask = (1u << p.bits[pass]) - 1u;
-  const int64_t seg = tile / p.tps;
-  const int tin = (int)(tile - seg * p.tps);
+  const int nbits = p.bits[pass];
+  const uint32_t mask = (1u << nbits) - 1u;
+  // tickets go round-robin over the segments (ticket = tin * nseg + seg): a
+  // tile's predecessor in its segment holds an earlier ticket, and the tiles in
+  // flight per segment -- the depth of a look-back walk -- are ~grid / nseg
+  const int64_t tin64 = ticket / p.nseg;
+  const int64_t seg = ticket - tin64 * p.nseg;
+  const int tin = (int)tin64;
+  const int64_t tile = seg * p.tps + tin;  // status row
+  if (pass + 1 < p.npass)
+    for (int d = t; d < RBINS; d += RT) p.status[(pass + 1) & 1][(size_t)tile * RBINS + d] = 0u;
   const int64_t sbase = seg * (int64_t)p.seg_len;
   const int in0 = tin * TILE;
   const int n = min(TILE, p.seg_len - in0);
@@ -227,36 +293,75 @@ __global__ void __launch_bounds__(RT) k_radix_pass(const __grid_constant__ Radix
   for (int i = t; i < RW * RBINS; i += RT) (&sm.whist[0][0])[i] = 0u;
   if (last && p.tokens && p.lanes <= TOK_SMEM)
     for (int i = t; i < p.lanes; i += RT) sm.tok[i] = 0;
-  __syncthreads();
 
-  // load (warp w owns keys [w*512, w*512+512) of the tile, lane-striped) and
-  // rank stably: inside a warp by (iteration, lane) = input order
+  // load (warp w owns keys [w*512, w*512+512) of the tile, lane-striped): every
+  // load of the tile is issued before the first use
   unsigned long long key[RI];
   int32_t pos[RI];
   uint32_t rank[RI];
+#pragma unroll
+  for (int j = 0; j < RI; ++j) {
+    const int i = w * WKEYS + j * 32 + lane;
+    const int64_t g = sbase + in0 + i;
+    key[j] = 0ull;
+    pos[j] = 0;
+    if (i < n) {
+      if (from_input) {
+        key[j] = make_key(p, __ldg(p.lens + g), __ldg(p.ids + g));
+        pos[j] = (int32_t)g;
+      } else {
+        key[j] = __ldcs(kin + g);
+        if constexpr (POS) pos[j] = __ldcs(pin + g);
+      }
+    }
+  }
+  // warm L2 with the tile a CTA of the next round will take (ticket + grid):
+  // one 128 B line per thread of the pass's input; the tile's own loads above
+  // are already in flight
+  {
+    const int64_t nt = ticket + gridDim.x;
+    if (nt < p.ntiles) {
+      const int64_t ntin = nt / p.nseg, nseg_ = nt - ntin * p.nseg;
+      const int nin0 = (int)ntin * TILE;
+      const int nn = min(TILE, p.seg_len - nin0);
+      const int64_t g0 = nseg_ * (int64_t)p.seg_len + nin0;
+      if (from_input) {  // 2 x 4 B per key: lens lines, then ids lines
+        const int per = 32;  // keys per 128 B line
+        const int lines = (nn + per - 1) / per;
+        if (t < lines) prefetch_l2(p.lens + g0 + t * per);
+        else if (t - lines < lines) prefetch_l2(p.ids + g0 + (t - lines) * per);
+      } else {  // 8 B keys
+        const int lines = (nn + 15) / 16;
+        for (int l = t; l < lines; l += RT) prefetch_l2(kin + g0 + l * 16);
+      }
+    }
+  }
+  __syncthreads();  // whist cleared
+  // rank stably: inside a warp by (iteration, lane) = input order.  The peer
+  // group's leader takes the group's slots with one shared atomic; a warp's
+  // atomics are performed in issue order, so the rounds need no barrier
+  // between them and their atomics pipeline.
   const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
   for (int j = 0; j < RI; ++j) {
     const int i = w * WKEYS + j * 32 + lane;
     const bool valid = i < n;
-    const int64_t g = sbase + in0 + i;
-    if (valid) {
-      if (from_input) {
-        key[j] = make_key(p, p.lens[g], p.ids[g]);
-        pos[j] = (int32_t)g;
-      } else {
-        key[j] = kin[g];
-        if constexpr (POS) pos[j] = pin[g];
+    const uint32_t d = valid ? (uint32_t)(key[j] >> shift) & mask : 0u;
+    // lanes with this lane's digit: one ballot per digit bit (MATCH.ANY costs a
+    // pass per distinct value, ~30 for a random 9-bit digit)
+    uint32_t peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+    for (int b = 0; b < RBITS; ++b) {
+      if (b < nbits) {
+        const bool bit = (d >> b) & 1u;
+        const uint32_t m = __ballot_sync(0xffffffffu, bit);
+        peers &= bit ? m : ~m;
       }
     }
-    const uint32_t d = valid ? (uint32_t)(key[j] >> shift) & mask : 0xffffffffu;
-    const uint32_t peers = __match_any_sync(0xffffffffu, d);
-    uint32_t cnt = 0;
-    if (valid) cnt = sm.whist[w][d];
-    __syncwarp();
-    if (valid && lane == __ffs(peers) - 1) sm.whist[w][d] = cnt + __popc(peers);
-    __syncwarp();
-    rank[j] = cnt + __popc(peers & lt);
+    const int leader = __ffs(peers) - 1;
+    uint32_t base = 0;
+    if (valid && lane == leader) base = atomicAdd(&sm.whist[w][d], (uint32_t)__popc(peers));
+    rank[j] = __shfl_sync(0xffffffffu, base, leader) + __popc(peers & lt);
   }
   __syncthreads();
 
@@ -320,6 +425,68 @@ __global__ void __launch_bounds__(RT) k_radix_pass(const __grid_constant__ Radix
   }
   __syncthreads();
 
+  // last pass: deal each key straight to its output slot (balance.py:59-70)
+  const unsigned long long idmask = (1ull << p.id_bits) - 1ull;
+  const bool tok_smem = p.tokens && p.lanes <= TOK_SMEM;
+  // q / lanes = umul64hi(q, floor(2^64 / lanes) + 1), exact for q * lanes < 2^64
+  const unsigned long long lanes_magic = ~0ull / (unsigned long long)p.lanes + 1ull;
+  // lanes of a warp that deal to the same GPU lane add their lengths first (one atomic per
+  // group); with lanes = 1 every key lands on one counter: a register sum
+  const bool tok_redux = p.max_len < (1 << 26);
+  unsigned long long tsum = 0;
+  auto deal = [&](bool v, unsigned long long k, int32_t pv, uint32_t q) {  // q: sorted slot in the segment
+    int ln = -1;
+    int32_t len = 0;
+    if (v) {
+      const uint32_t r = p.lanes == 1 ? q : (uint32_t)__umul64hi((unsigned long long)q, lanes_magic);
+      const int c = (int)(q - r * (uint32_t)p.lanes);
+      ln = (p.snake && (r & 1u)) ? p.lanes - 1 - c : c;  // balance.py:66-67
+      const int64_t o = sbase + (int64_t)ln * p.rows + r;
+      B2_DASSERT(ln >= 0 && ln < p.lanes && (int)r < p.rows);
+      p.out_ids[o] = (int32_t)(k & idmask);
+      if constexpr (POS) p.out_pos[o] = pv;
+      len = p.max_len - (int32_t)(k >> p.id_bits);
+    }
+    if (!p.tokens) return;
+    if (p.lanes == 1) {
+      tsum += (unsigned long long)len;
+    } else if (tok_redux) {
+      const unsigned grp = __match_any_sync(0xffffffffu, ln);
+      const unsigned sum = __reduce_add_sync(grp, (unsigned)len);
+      if (v && lane == __ffs(grp) - 1) {
+        if (tok_smem) atomicAdd(reinterpret_cast<unsigned long long*>(&sm.tok[ln]), (unsigned long long)sum);
+        else atomicAdd(reinterpret_cast<unsigned long long*>(&p.tokens[seg * p.lanes + ln]), (unsigned long long)sum);
+      }
+    } else if (v) {
+      if (tok_smem) atomicAdd(reinterpret_cast<unsigned long long*>(&sm.tok[ln]), (unsigned long long)len);
+      else atomicAdd(reinterpret_cast<unsigned long long*>(&p.tokens[seg * p.lanes + ln]), (unsigned long long)len);
+    }
+  };
+  auto flush_tokens = [&]() {
+    if (p.tokens && p.lanes == 1) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) tsum += __shfl_xor_sync(0xffffffffu, tsum, o);
+      if (lane == 0 && tsum) atomicAdd(reinterpret_cast<unsigned long long*>(&p.tokens[seg]), tsum);
+    } else if (tok_smem) {
+      __syncthreads();
+      for (int l = t; l < p.lanes; l += RT)  // per-lane token sums (_from_per_gpu, balance.py:54-56)
+        if (sm.tok[l]) atomicAdd(reinterpret_cast<unsigned long long*>(&p.tokens[seg * p.lanes + l]), (unsigned long long)sm.tok[l]);
+    }
+  };
+#ifdef B2_K5_DIRECT
+  if (last) {  // each key knows its slot: gbase + the warp's prefix + its rank; no staging
+#pragma unroll
+    for (int j = 0; j < RI; ++j) {
+      const int i = w * WKEYS + j * 32 + lane;
+      const bool v = i < n;
+      const uint32_t d = (uint32_t)(key[j] >> shift) & mask;
+      deal(v, key[j], pos[j], v ? sm.gbase[d] + sm.whist[w][d] + rank[j] : 0u);
+    }
+    flush_tokens();
+    return;
+  }
+#endif
+
   // stage the tile digit-sorted
 #pragma unroll
   for (int j = 0; j < RI; ++j) {
@@ -347,49 +514,41 @@ __global__ void __launch_bounds__(RT) k_radix_pass(const __grid_constant__ Radix
     }
     return;
   }
-  // last pass: deal straight from the sorted slot (balance.py:59-70)
-  const unsigned long long idmask = (1ull << p.id_bits) - 1ull;
-  const bool tok_smem = p.tokens && p.lanes <= TOK_SMEM;
-  // q / lanes = umul64hi(q, floor(2^64 / lanes) + 1), exact for q * lanes < 2^64
-  const unsigned long long lanes_magic = ~0ull / (unsigned long long)p.lanes + 1ull;
-  // lanes of a warp that deal to the same GPU lane add their lengths first (one atomic per
-  // group; with lanes = 1 every key of the tile lands on one counter)
-  const bool tok_redux = p.max_len < (1 << 26);
   for (int i0 = 0; i0 < n; i0 += RT) {
     const int i = i0 + t;
     const bool v = i < n;
-    int ln = -1;
-    int32_t len = 0;
+    unsigned long long k = 0ull;
+    uint32_t q = 0u;
+    int32_t pv = 0;
     if (v) {
-      const unsigned long long k = sm.key[i];
+      k = sm.key[i];
       const uint32_t d = (uint32_t)(k >> shift) & mask;
-      const int64_t q = (int64_t)sm.gbase[d] + (i - sm.off[d]);  // sorted slot inside the segment
-      const int64_t r = p.lanes == 1 ? q : (int64_t)__umul64hi((unsigned long long)q, lanes_magic);
-      const int c = (int)(q - r * p.lanes);
-      ln = (p.snake && (r & 1)) ? p.lanes - 1 - c : c;  // balance.py:66-67
-      const int64_t o = sbase + (int64_t)ln * p.rows + r;
-      B2_DASSERT(ln >= 0 && ln < p.lanes && r >= 0 && r < p.rows);
-      p.out_ids[o] = (int32_t)(k & idmask);
-      if constexpr (POS) p.out_pos[o] = sm.pos[i];
-      len = p.max_len - (int32_t)(k >> p.id_bits);
+      q = sm.gbase[d] + (uint32_t)(i - sm.off[d]);
+      if constexpr (POS) pv = sm.pos[i];
     }
-    if (!p.tokens) continue;
-    if (tok_redux) {
-      const unsigned grp = __match_any_sync(0xffffffffu, ln);
-      const unsigned sum = __reduce_add_sync(grp, (unsigned)len);
-      if (v && lane == __ffs(grp) - 1) {
-        if (tok_smem) atomicAdd(reinterpret_cast<unsigned long long*>(&sm.tok[ln]), (unsigned long long)sum);
-        else atomicAdd(reinterpret_cast<unsigned long long*>(&p.tokens[seg * p.lanes + ln]), (unsigned long long)sum);
-      }
-    } else if (v) {
-      if (tok_smem) atomicAdd(reinterpret_cast<unsigned long long*>(&sm.tok[ln]), (unsigned long long)len);
-      else atomicAdd(reinterpret_cast<unsigned long long*>(&p.tokens[seg * p.lanes + ln]), (unsigned long long)len);
-    }
+    deal(v, k, pv, q);
   }
-  if (tok_smem) {
+  flush_tokens();
+}
+
+// Persistent: grid = resident CTAs; each CTA takes tiles by atomic ticket
+// until none are left (ticket order = look-back order, so a predecessor tile
+// is always held by a running CTA).  A skipped pass costs one flag read per CTA.
+template <bool POS>
+__global__ void __launch_bounds__(RT, 3) k_radix_pass(const __grid_constant__ RadixParams p, int pass) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PassSmem<POS>& sm = *reinterpret_cast<PassSmem<POS>*>(smem_raw);
+  pdl_wait();     // the previous pass (or the upsweep) has completed and its writes are visible
+  pdl_trigger();  // the next pass may launch; it waits for this grid in turn
+  const bool unsorted = *(volatile const int32_t*)p.flags != 0;
+  if (!unsorted && pass < p.npass_id) return;  // ids already ordered: length passes only
+  for (;;) {
+    __syncthreads();  // the previous tile's shared-memory reads are done
+    if (threadIdx.x == 0) sm.tile = (int)atomicAdd(&p.counters[pass], 1u);
     __syncthreads();
-    for (int l = t; l < p.lanes; l += RT)  // per-lane token sums (_from_per_gpu, balance.py:54-56)
-      if (sm.tok[l]) atomicAdd(reinterpret_cast<unsigned long long*>(&p.tokens[seg * p.lanes + l]), (unsigned long long)sm.tok[l]);
+    const int64_t ticket = sm.tile;
+    if (ticket >= p.ntiles) return;
+    radix_tile<POS>(p, pass, unsorted, ticket, sm);
   }
 }
 
@@ -530,20 +689,29 @@ extern "C" int b2_presort_sort_deal(const int32_t* ids, const int32_t* lens, int
   const int64_t ctas = std::min<int64_t>(pl.ntiles, (int64_t)di.sm_count * 4);
   const int64_t per = (pl.ntiles + ctas - 1) / ctas;
   const int64_t grid_up = (pl.ntiles + per - 1) / per;
-  k_radix_upsweep<<<(unsigned)grid_up, RT, 0, st>>>(p, per);
+  k_radix_hist<false><<<(unsigned)grid_up, RT, 0, st>>>(p, per);
   B2_CHECK(cudaGetLastError());
+  if (pl.npass_id > 0) B2_CHECK(launch_pdl(k_radix_hist<true>, dim3((unsigned)grid_up), dim3(RT), 0, st, p, per));
   const size_t smem = out_pos ? sizeof(PassSmem<true>) : sizeof(PassSmem<false>);
-  static bool configured[64][2] = {};
+  static int occ_cached[64][2] = {};
   const bool pos = out_pos != nullptr;
-  if (!configured[di.device & 63][pos]) {
-    if (pos) B2_CHECK(cudaFuncSetAttribute((const void*)k_radix_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    else B2_CHECK(cudaFuncSetAttribute((const void*)k_radix_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured[di.device & 63][pos] = true;
+  int& occ = occ_cached[di.device & 63][pos];
+  if (occ == 0) {
+    if (pos) {
+      B2_CHECK(cudaFuncSetAttribute((const void*)k_radix_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      B2_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_radix_pass<true>, RT, smem));
+    } else {
+      B2_CHECK(cudaFuncSetAttribute((const void*)k_radix_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      B2_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_radix_pass<false>, RT, smem));
+    }
+    B2_REQUIRE(occ >= 1, B2_ERR_CUDA, "radix pass cannot be resident");
   }
+  // persistent: one wave of resident CTAs takes the tiles by ticket
+  const unsigned grid = (unsigned)std::min<int64_t>(pl.ntiles, (int64_t)di.sm_count * occ);
   for (int q = 0; q < pl.npass; ++q) {
     // programmatic dependents: each pass launches under the previous kernel's tail
-    if (pos) B2_CHECK(launch_pdl(k_radix_pass<true>, dim3((unsigned)pl.ntiles), dim3(RT), smem, st, p, q));
-    else B2_CHECK(launch_pdl(k_radix_pass<false>, dim3((unsigned)pl.ntiles), dim3(RT), smem, st, p, q));
+    if (pos) B2_CHECK(launch_pdl(k_radix_pass<true>, dim3(grid), dim3(RT), smem, st, p, q));
+    else B2_CHECK(launch_pdl(k_radix_pass<false>, dim3(grid), dim3(RT), smem, st, p, q));
     B2_CHECK(cudaGetLastError());
   }
   return B2_OK;
