@@ -161,6 +161,7 @@ __global__ void __launch_bounds__(RT, 4) k_radix_hist(const __grid_constant__ Ra
   __shared__ uint32_t s_h[MAX_PASS][RBINS];
   __shared__ int s_unsorted;
   const int t = threadIdx.x, lane = t & 31;
+  static_assert(UKEYS * 32 == WKEYS, "a warp covers its 512 keys in UKEYS rounds");
   if constexpr (IDS) {
     pdl_wait();  // the upsweep's sortedness flag
     pdl_trigger();
@@ -207,40 +208,55 @@ __global__ void __launch_bounds__(RT, 4) k_radix_hist(const __grid_constant__ Ra
     const int64_t sbase = seg * (int64_t)p.seg_len;
     const int in0 = (int)(tile - seg * p.tps) * TILE;
     const int n = min(TILE, p.seg_len - in0);
+    // warp w owns keys [w*512, w*512+512) of the tile, lane-striped rounds:
+    // the key after lane 31's is lane 0's of the next round (a shuffle)
+    const int w = t >> 5;
     int32_t L[UKEYS], D[UKEYS];
     const uint64_t pol = policy_evict_last();
+    const int32_t* idp = p.ids + sbase + in0 + w * WKEYS + lane;
+    const int32_t* lnp = p.lens + sbase + in0 + w * WKEYS + lane;
+    const int nw = n - w * WKEYS;  // keys of this warp (may be <= 0)
 #pragma unroll
-    for (int j = 0; j < UKEYS; ++j) {  // striped: coalesced, all loads in flight
-      const int i = j * RT + t;
+    for (int j = 0; j < UKEYS; ++j) {  // coalesced, all loads in flight
       L[j] = 1;
       D[j] = 0;
-      if (i < n) {
+      if (j * 32 + lane < nw) {
         if constexpr (IDS) {
-          D[j] = __ldg(p.ids + sbase + in0 + i);
+          D[j] = __ldg(idp + j * 32);
         } else {
-          D[j] = ld_keep(p.ids + sbase + in0 + i, pol);
-          L[j] = ld_keep(p.lens + sbase + in0 + i, pol);
+          D[j] = ld_keep(idp + j * 32, pol);
+          L[j] = ld_keep(lnp + j * 32, pol);
         }
       }
     }
+    if constexpr (!IDS) {
+      // the key after the warp's last: the next warp's / tile's first (an L1/L2 hit)
+      const int last_i = in0 + w * WKEYS + min(nw, WKEYS);  // in-segment index after the warp's keys
+      const int32_t after = (nw > 0 && last_i < p.seg_len) ? __ldg(p.ids + sbase + last_i) : 0x7fffffff;
 #pragma unroll
-    for (int j = 0; j < UKEYS; ++j) {
-      const int i = j * RT + t;
-      const bool valid = i < n;
-      if constexpr (!IDS) {
-        const int64_t g = sbase + in0 + i;
-        // the next key's id: lane+1's, or (lane 31 / the tile's last key) one load that hits L1/L2
-        int32_t nxt = __shfl_down_sync(0xffffffffu, D[j], 1);
-        if (valid && (lane == 31 || i + 1 >= n)) nxt = in0 + i + 1 < p.seg_len ? __ldg(p.ids + g + 1) : 0x7fffffff;
+      for (int j = 0; j < UKEYS; ++j) {
+        const int iw = j * 32 + lane;
+        const bool valid = iw < nw;
+        const int32_t nx0 = __shfl_down_sync(0xffffffffu, D[j], 1);
+        const int32_t nx1 = __shfl_sync(0xffffffffu, j + 1 < UKEYS ? D[j + 1 < UKEYS ? j + 1 : j] : 0, 0);
+        int32_t nxt = lane < 31 ? nx0 : (j + 1 < UKEYS ? nx1 : after);
+        if (iw + 1 == nw) nxt = after;  // the warp's last key
         if (valid) {
-          if (!(L[j] >= 1 && L[j] <= p.max_len && D[j] >= 0 && D[j] <= p.max_id) && first_bad < 0) first_bad = g;
+          if (!(L[j] >= 1 && L[j] <= p.max_len && D[j] >= 0 && D[j] <= p.max_id) && first_bad < 0)
+            first_bad = sbase + in0 + w * WKEYS + iw;
           if (nxt < D[j]) unsorted = 1;
+          // length digits from 32-bit arithmetic: shift >= id_bits for every length pass
+          const uint32_t lk = (uint32_t)(p.max_len - (L[j] < 1 ? 1 : (L[j] > p.max_len ? p.max_len : L[j])));
+          for (int q = q0; q < q1; ++q) atomicAdd(&s_h[q][(lk >> (p.shift[q] - p.id_bits)) & ((1u << p.bits[q]) - 1u)], 1u);
         }
       }
-      if (valid) {
-        const unsigned long long k = make_key(p, L[j], D[j]);
-        for (int q = q0; q < q1; ++q) atomicAdd(&s_h[q][(uint32_t)(k >> p.shift[q]) & ((1u << p.bits[q]) - 1u)], 1u);
-      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < UKEYS; ++j)
+        if (j * 32 + lane < nw) {
+          const uint32_t dk = (uint32_t)(D[j] < 0 ? 0 : (D[j] > p.max_id ? p.max_id : D[j]));
+          for (int q = q0; q < q1; ++q) atomicAdd(&s_h[q][(dk >> p.shift[q]) & ((1u << p.bits[q]) - 1u)], 1u);
+        }
     }
   }
   if constexpr (!IDS) {
@@ -686,7 +702,7 @@ extern "C" int b2_presort_sort_deal(const int32_t* ids, const int32_t* lens, int
   B2_CHECK(cudaMemsetAsync(ws + pl.off_hist, 0, (size_t)pl.npass * nseg * RBINS * 4, st));
   B2_CHECK(cudaMemsetAsync(ws + pl.off_flags, 0, 16, st));
   const DeviceInfo& di = device_info();
-  const int64_t ctas = std::min<int64_t>(pl.ntiles, (int64_t)di.sm_count * 4);
+  const int64_t ctas = std::min<int64_t>(pl.ntiles, (int64_t)di.sm_count * 8);
   const int64_t per = (pl.ntiles + ctas - 1) / ctas;
   const int64_t grid_up = (pl.ntiles + per - 1) / per;
   k_radix_hist<false><<<(unsigned)grid_up, RT, 0, st>>>(p, per);
