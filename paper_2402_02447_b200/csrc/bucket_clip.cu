@@ -53,6 +53,12 @@ __global__ void __launch_bounds__(THREADS, CPS) k_bucket_clip_l2lag(const __grid
                                         double, float>::type;
   __shared__ double s_coef[2];
   __shared__ double red[32];
+  // lone-bucket launches are programmatic dependents (launch_l2lag): the
+  // launch overlaps the previous kernel's tail, every read waits for it.  A
+  // no-op otherwise.  Triggering here is safe: a dependent can only start once
+  // every CTA of this grid has triggered, i.e. is resident.
+  pdl_wait();
+  pdl_trigger();
   const int G = gridDim.x, c = blockIdx.x, t = threadIdx.x;
   const bool scale = p.out != nullptr;
   const uint64_t pol_keep = scale ? l2_policy_evict_last() : l2_policy_evict_first();
@@ -252,8 +258,24 @@ int launch_l2lag(ClipParams& p, cudaStream_t stream) {
   cfg.dynamicSmemBytes = 0;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;  // CTAs wait on each other's partials
-  attr[0].val.cooperative = 1;
+  // A lone bucket (the DDP-hook / reducer shape, one launch per bucket) is
+  // launch-bound: it goes out as a programmatic dependent launch, which a
+  // cooperative launch cannot be (~2 us of the 12 us; DESIGN K1).  The grid
+  // is sized to what is co-resident, and a dependent of this grid can only
+  // start once all of its CTAs are resident, so the spin on the partials
+  // still sees every CTA.  Several buckets per launch stay cooperative.
+  static int pdl_env = -1;
+  if (pdl_env < 0) {
+    const char* e = getenv("B2_CLIP_PDL");
+    pdl_env = e ? atoi(e) : 1;
+  }
+  if (p.nseg == 1 && p.out != nullptr && pdl_env) {
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+  } else {
+    attr[0].id = cudaLaunchAttributeCooperative;  // CTAs wait on each other's partials
+    attr[0].val.cooperative = 1;
+  }
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   B2_CHECK(cudaLaunchKernelEx(&cfg, kern, p));

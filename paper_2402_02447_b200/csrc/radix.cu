@@ -58,7 +58,7 @@ constexpr int WKEYS = TILE / RW;   // 512 keys per warp
 constexpr int RBITS = 9;           // widest digit
 constexpr int RBINS = 1 << RBITS;  // 512 bins
 constexpr int MAX_PASS = 8;
-constexpr int TOK_SMEM = 1024;     // lanes whose token sums are staged in shared memory
+constexpr int TOK_SMEM = 256;      // lanes whose token sums are staged in shared memory
 constexpr int kLookBack = 16;      // predecessor status words per look-back round trip
 
 constexpr uint32_t ST_AGG = 1u << 30, ST_PRE = 2u << 30, ST_VAL = (1u << 30) - 1u;
@@ -274,7 +274,12 @@ template <bool POS>
 struct PassSmem {
   unsigned long long key[TILE];  // tile, digit-sorted
   int32_t pos[POS ? TILE : 1];
-  uint32_t whist[RW][RBINS];     // per-warp digit counts, then per-warp exclusive prefixes
+  // per-warp digit counts, then per-warp exclusive prefixes: 16-bit fields
+  // (<= 4096 per tile), two per 32-bit word for the ranking atomics
+  union {
+    uint16_t whist[RW][RBINS];
+    uint32_t whist2[RW][RBINS / 2];
+  };
   uint32_t off[RBINS];           // tile-local digit starts
   uint32_t gbase[RBINS];         // global (segment) offset of this tile's first key of each digit
   long long tok[TOK_SMEM];       // per-lane token sums of this tile (last pass)
@@ -306,7 +311,7 @@ __device__ __forceinline__ void radix_tile(const RadixParams& p, int pass, bool 
   const unsigned long long* kin = p.keys[(exec - 1) & 1];
   const int32_t* pin = p.pos[(exec - 1) & 1];
 
-  for (int i = t; i < RW * RBINS; i += RT) (&sm.whist[0][0])[i] = 0u;
+  for (int i = t; i < RW * RBINS / 2; i += RT) (&sm.whist2[0][0])[i] = 0u;
   if (last && p.tokens && p.lanes <= TOK_SMEM)
     for (int i = t; i < p.lanes; i += RT) sm.tok[i] = 0;
 
@@ -376,7 +381,8 @@ __device__ __forceinline__ void radix_tile(const RadixParams& p, int pass, bool 
     }
     const int leader = __ffs(peers) - 1;
     uint32_t base = 0;
-    if (valid && lane == leader) base = atomicAdd(&sm.whist[w][d], (uint32_t)__popc(peers));
+    if (valid && lane == leader)
+      base = (atomicAdd(&sm.whist2[w][d >> 1], (uint32_t)__popc(peers) << (16 * (d & 1))) >> (16 * (d & 1))) & 0xffffu;
     rank[j] = __shfl_sync(0xffffffffu, base, leader) + __popc(peers & lt);
   }
   __syncthreads();
@@ -392,7 +398,7 @@ __device__ __forceinline__ void radix_tile(const RadixParams& p, int pass, bool 
 #pragma unroll
     for (int ww = 0; ww < RW; ++ww) {
       const uint32_t c = sm.whist[ww][d];
-      sm.whist[ww][d] = run;
+      sm.whist[ww][d] = (uint16_t)run;
       run += c;
     }
     tot[h] = run;
@@ -551,7 +557,7 @@ __device__ __forceinline__ void radix_tile(const RadixParams& p, int pass, bool 
 // until none are left (ticket order = look-back order, so a predecessor tile
 // is always held by a running CTA).  A skipped pass costs one flag read per CTA.
 template <bool POS>
-__global__ void __launch_bounds__(RT, 3) k_radix_pass(const __grid_constant__ RadixParams p, int pass) {
+__global__ void __launch_bounds__(RT, 4) k_radix_pass(const __grid_constant__ RadixParams p, int pass) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PassSmem<POS>& sm = *reinterpret_cast<PassSmem<POS>*>(smem_raw);
   pdl_wait();     // the previous pass (or the upsweep) has completed and its writes are visible

@@ -404,6 +404,43 @@ def test_lone_bucket_hook_shape(n, shift, scale):
     assert flags.item() == 1
 
 
+def test_lone_bucket_launches_back_to_back():
+    """The reducer / DDP-hook pattern: one K1 launch per bucket, each a programmatic dependent
+    launch of the previous one (they share the clip workspace counters).  26 buckets of mixed
+    scale back to back, eagerly and replayed from a CUDA graph, on a side stream: every bucket's
+    coefficient and clipped values vs the oracle, graph == eager bit for bit."""
+    rng = np.random.default_rng(11)
+    sizes = [int(s) for s in rng.integers(200_000, 1_500_000, size=26)]
+    scales = [10.0 ** float(e) for e in rng.uniform(-5, -1, size=26)]
+    x = np.concatenate([rng.normal(size=n) * sc for n, sc in zip(sizes, scales)]).astype(np.float32)
+    layout, a = [], 0
+    for n in sizes:
+        layout.append((a, a + n))
+        a += n
+    g = torch.from_numpy(x).cuda()
+    lim = 1.0 / np.sqrt(len(layout))
+    _, rc = O.bucket_coefficients(x.astype(np.float64), layout, lim)
+    ref = np.concatenate([x[s:e].astype(np.float64) * rc[b] for b, (s, e) in enumerate(layout)])
+    c = BucketClipper()
+    side = torch.cuda.Stream()
+    out = torch.empty_like(g)
+    with torch.cuda.stream(side):
+        for s, e in reversed(layout):  # backward order
+            c.clip_cast(g, out, [(s, s, e - s)], lim)
+    side.synchronize()
+    assert rel_err(out.cpu().numpy(), ref) <= F32_REL
+    out2 = torch.zeros_like(g)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=side):
+        for s, e in reversed(layout):
+            c.clip_cast(g, out2, [(s, s, e - s)], lim)
+    for _ in range(3):
+        out2.zero_()
+        graph.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out2, out)
+
+
 def test_gradient_state_staged_host_copy_is_exact():
     """A large pageable numpy state goes to the device through the pinned staging ring
     (gradsync._staged_h2d: several slots, host threads, ragged last slot): bit-exact copy,
