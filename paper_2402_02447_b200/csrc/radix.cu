@@ -75,6 +75,8 @@ struct RadixParams {
   int shift[MAX_PASS], bits[MAX_PASS];
   uint32_t* hist;       // [npass][nseg][RBINS]
   uint32_t* status[2];  // [ntiles][RBINS] look-back words, alternating by pass
+  uint16_t* tcnt;       // [ntiles][RBINS] first length digit per tile, input order (upsweep)
+  uint32_t* tbase;      // [ntiles][RBINS] its tile bases in the segment (k_radix_tscan)
   uint32_t* counters;   // [MAX_PASS] tile tickets
   int32_t* flags;       // [0]: 1 if some segment's ids decrease somewhere
   unsigned long long* keys[2];
@@ -159,6 +161,7 @@ static_assert(UKEYS * RT == TILE, "one upsweep round covers a tile");
 template <bool IDS>
 __global__ void __launch_bounds__(RT, 4) k_radix_hist(const __grid_constant__ RadixParams p, int64_t tiles_per_cta) {
   __shared__ uint32_t s_h[MAX_PASS][RBINS];
+  __shared__ uint32_t s_t[IDS ? 1 : RBINS];  // this tile's first length digit (-> tcnt)
   __shared__ int s_unsorted;
   const int t = threadIdx.x, lane = t & 31;
   static_assert(UKEYS * 32 == WKEYS, "a warp covers its 512 keys in UKEYS rounds");
@@ -182,6 +185,8 @@ __global__ void __launch_bounds__(RT, 4) k_radix_hist(const __grid_constant__ Ra
     if (t == 0) s_unsorted = 0;
   }
   for (int i = t; i < MAX_PASS * RBINS; i += RT) (&s_h[0][0])[i] = 0u;
+  if constexpr (!IDS)
+    for (int i = t; i < RBINS; i += RT) s_t[i] = 0u;
   __syncthreads();
   auto flush = [&](int64_t seg) {
     for (int i = q0 * RBINS + t; i < q1 * RBINS; i += RT) {
@@ -247,9 +252,20 @@ __global__ void __launch_bounds__(RT, 4) k_radix_hist(const __grid_constant__ Ra
           if (nxt < D[j]) unsorted = 1;
           // length digits from 32-bit arithmetic: shift >= id_bits for every length pass
           const uint32_t lk = (uint32_t)(p.max_len - (L[j] < 1 ? 1 : (L[j] > p.max_len ? p.max_len : L[j])));
-          for (int q = q0; q < q1; ++q) atomicAdd(&s_h[q][(lk >> (p.shift[q] - p.id_bits)) & ((1u << p.bits[q]) - 1u)], 1u);
+          atomicAdd(&s_t[(lk >> (p.shift[q0] - p.id_bits)) & ((1u << p.bits[q0]) - 1u)], 1u);
+          for (int q = q0 + 1; q < q1; ++q) atomicAdd(&s_h[q][(lk >> (p.shift[q] - p.id_bits)) & ((1u << p.bits[q]) - 1u)], 1u);
         }
       }
+      // the tile's first-length-digit counts: to tcnt (the ordered-ids fast path's
+      // tile bases, k_radix_tscan) and into the segment histogram
+      __syncthreads();
+      for (int b = t; b < RBINS; b += RT) {
+        const uint32_t c = s_t[b];
+        p.tcnt[(size_t)tile * RBINS + b] = (uint16_t)c;
+        s_h[q0][b] += c;
+        s_t[b] = 0u;
+      }
+      __syncthreads();
     } else {
 #pragma unroll
       for (int j = 0; j < UKEYS; ++j)
@@ -267,6 +283,61 @@ __global__ void __launch_bounds__(RT, 4) k_radix_hist(const __grid_constant__ Ra
   if (cur_seg >= 0) flush(cur_seg);
   if constexpr (!IDS)
     if (t == 0 && s_unsorted) atomicOr(p.flags, 1);
+}
+
+// ---------------------------------------------------------------- tile bases
+// Ids already ordered (the first length pass reads the input order the upsweep
+// counted): every tile's per-digit base in its segment is known before the
+// pass, so the pass needs no look-back.  CTA (segment, 32 digits), 1024
+// threads: warp w sums its run of tiles per digit (lane), the runs are
+// scanned in shared memory, then each run is walked again writing bases.
+constexpr int TS_T = 1024, TS_W = TS_T / 32;
+__global__ void __launch_bounds__(TS_T) k_radix_tscan(const __grid_constant__ RadixParams p) {
+  pdl_wait();
+  pdl_trigger();
+  if (*(volatile const int32_t*)p.flags != 0) return;  // ids decrease somewhere: look-back passes
+  __shared__ uint32_t s_run[TS_W][32];
+  __shared__ uint32_t s_tot[RBINS];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t seg = blockIdx.x / (RBINS / 32);
+  const int d = (int)(blockIdx.x % (RBINS / 32)) * 32 + lane;
+  const int q = p.npass_id;  // the first length pass
+  const uint32_t* hseg = p.hist + ((size_t)q * p.nseg + seg) * RBINS;
+  const int per = (p.tps + TS_W - 1) / TS_W;
+  const int k0 = min(w * per, p.tps), k1 = min(k0 + per, p.tps);
+  const uint16_t* tc = p.tcnt + (size_t)seg * p.tps * RBINS + d;
+  uint32_t sum = 0;
+#pragma unroll 8
+  for (int k = k0; k < k1; ++k) sum += tc[(size_t)k * RBINS];
+  s_run[w][lane] = sum;
+  if (w == 0) {  // exclusive prefix of the segment's digit totals: 16 per lane + a warp scan
+    uint32_t v[RBINS / 32], run = 0;
+#pragma unroll
+    for (int i = 0; i < RBINS / 32; ++i) {
+      v[i] = hseg[lane * (RBINS / 32) + i];
+      run += v[i];
+    }
+    uint32_t x = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    x -= run;
+#pragma unroll
+    for (int i = 0; i < RBINS / 32; ++i) {
+      s_tot[lane * (RBINS / 32) + i] = x;
+      x += v[i];
+    }
+  }
+  __syncthreads();
+  uint32_t base = s_tot[d];  // digits before d in the segment (the sort is by digit first)
+  for (int i = 0; i < w; ++i) base += s_run[i][lane];
+  uint32_t* tb = p.tbase + (size_t)seg * p.tps * RBINS + d;
+  for (int k = k0; k < k1; ++k) {
+    tb[(size_t)k * RBINS] = base;
+    base += tc[(size_t)k * RBINS];
+  }
 }
 
 // ---------------------------------------------------------------- onesweep pass
@@ -405,15 +476,29 @@ __device__ __forceinline__ void radix_tile(const RadixParams& p, int pass, bool 
   }
   // publish this tile's per-digit counts (the first tile of a segment has its
   // inclusive prefix at once)
+  // ids ordered and this is the first length pass: the tile bases are tabled
+  // (k_radix_tscan), no publish and no look-back
+  const bool tabled = !unsorted && pass == p.npass_id;
   uint32_t* st = p.status[pass & 1] + (size_t)tile * RBINS;
+  uint32_t h0 = 0, h1 = 0, tb0 = 0, tb1 = 0;
+  if (tabled) {
+    tb0 = p.tbase[(size_t)tile * RBINS + 2 * t];
+    tb1 = p.tbase[(size_t)tile * RBINS + 2 * t + 1];
+  } else {
 #pragma unroll
-  for (int h = 0; h < 2; ++h) st_relaxed_u32(&st[2 * t + h], (tin == 0 ? ST_PRE : ST_AGG) | tot[h]);
-  const uint32_t* hseg = p.hist + ((size_t)pass * p.nseg + seg) * RBINS;
-  const uint32_t h0 = hseg[2 * t], h1 = hseg[2 * t + 1];
+    for (int h = 0; h < 2; ++h) st_relaxed_u32(&st[2 * t + h], (tin == 0 ? ST_PRE : ST_AGG) | tot[h]);
+    const uint32_t* hseg = p.hist + ((size_t)pass * p.nseg + seg) * RBINS;
+    h0 = hseg[2 * t];
+    h1 = hseg[2 * t + 1];
+  }
   uint32_t eloc, eglob;
   block_scan2(tot[0], tot[1], h0, h1, eloc, eglob, sm.warp_tot);
   sm.off[2 * t] = eloc;
   sm.off[2 * t + 1] = eloc + tot[0];
+  if (tabled) {
+    sm.gbase[2 * t] = tb0;
+    sm.gbase[2 * t + 1] = tb1;
+  } else {
   // decoupled look-back over the preceding tiles of this segment, kLookBack
   // predecessors per round trip (their status words are loaded together, then
   // folded newest-first until an inclusive prefix is met; an unpublished
@@ -444,6 +529,7 @@ __device__ __forceinline__ void radix_tile(const RadixParams& p, int pass, bool 
       st_relaxed_u32(&st[d], ST_PRE | (excl + tot[h]));
     }
     sm.gbase[d] = (eglob + (h ? h0 : 0u)) + excl;
+  }
   }
   __syncthreads();
 
@@ -587,7 +673,7 @@ struct Plan {
   int shift[MAX_PASS], bits[MAX_PASS];
   int tps;
   int64_t ntiles, n;
-  size_t off_keys[2], off_pos[2], off_hist, off_status[2], off_counters, off_flags, total;
+  size_t off_keys[2], off_pos[2], off_hist, off_status[2], off_tcnt, off_tbase, off_counters, off_flags, total;
 };
 
 // digits of <= 9 bits: the id bits first (LSD), then the length bits
@@ -630,6 +716,10 @@ bool make_plan(Plan& pl, int64_t nseg, int seg_len, int32_t max_len, int32_t max
     pl.off_status[b] = o;
     o = align256(o + (size_t)pl.ntiles * RBINS * 4);
   }
+  pl.off_tcnt = o;
+  o = align256(o + (size_t)pl.ntiles * RBINS * 2);
+  pl.off_tbase = o;
+  o = align256(o + (size_t)pl.ntiles * RBINS * 4);
   pl.off_counters = o;
   o = align256(o + MAX_PASS * 4);
   pl.off_flags = o;
@@ -695,6 +785,8 @@ extern "C" int b2_presort_sort_deal(const int32_t* ids, const int32_t* lens, int
     p.keys[b] = reinterpret_cast<unsigned long long*>(ws + pl.off_keys[b]);
     p.pos[b] = out_pos ? reinterpret_cast<int32_t*>(ws + pl.off_pos[b]) : nullptr;
   }
+  p.tcnt = reinterpret_cast<uint16_t*>(ws + pl.off_tcnt);
+  p.tbase = reinterpret_cast<uint32_t*>(ws + pl.off_tbase);
   p.counters = reinterpret_cast<uint32_t*>(ws + pl.off_counters);
   p.flags = reinterpret_cast<int32_t*>(ws + pl.off_flags);
   p.lanes = lanes;
@@ -714,6 +806,7 @@ extern "C" int b2_presort_sort_deal(const int32_t* ids, const int32_t* lens, int
   k_radix_hist<false><<<(unsigned)grid_up, RT, 0, st>>>(p, per);
   B2_CHECK(cudaGetLastError());
   if (pl.npass_id > 0) B2_CHECK(launch_pdl(k_radix_hist<true>, dim3((unsigned)grid_up), dim3(RT), 0, st, p, per));
+  B2_CHECK(launch_pdl(k_radix_tscan, dim3((unsigned)(nseg * (RBINS / 32))), dim3(TS_T), 0, st, p));
   const size_t smem = out_pos ? sizeof(PassSmem<true>) : sizeof(PassSmem<false>);
   static int occ_cached[64][2] = {};
   const bool pos = out_pos != nullptr;
