@@ -161,7 +161,7 @@ static_assert(UKEYS * RT == TILE, "one upsweep round covers a tile");
 template <bool IDS>
 __global__ void __launch_bounds__(RT, 4) k_radix_hist(const __grid_constant__ RadixParams p, int64_t tiles_per_cta) {
   __shared__ uint32_t s_h[MAX_PASS][RBINS];
-  __shared__ uint32_t s_t[IDS ? 1 : RBINS];  // this tile's first length digit (-> tcnt)
+  __shared__ uint32_t s_t[RBINS];  // this tile's counts of the first executed digit (-> tcnt)
   __shared__ int s_unsorted;
   const int t = threadIdx.x, lane = t & 31;
   static_assert(UKEYS * 32 == WKEYS, "a warp covers its 512 keys in UKEYS rounds");
@@ -185,8 +185,7 @@ __global__ void __launch_bounds__(RT, 4) k_radix_hist(const __grid_constant__ Ra
     if (t == 0) s_unsorted = 0;
   }
   for (int i = t; i < MAX_PASS * RBINS; i += RT) (&s_h[0][0])[i] = 0u;
-  if constexpr (!IDS)
-    for (int i = t; i < RBINS; i += RT) s_t[i] = 0u;
+  for (int i = t; i < RBINS; i += RT) s_t[i] = 0u;
   __syncthreads();
   auto flush = [&](int64_t seg) {
     for (int i = q0 * RBINS + t; i < q1 * RBINS; i += RT) {
@@ -256,24 +255,26 @@ __global__ void __launch_bounds__(RT, 4) k_radix_hist(const __grid_constant__ Ra
           for (int q = q0 + 1; q < q1; ++q) atomicAdd(&s_h[q][(lk >> (p.shift[q] - p.id_bits)) & ((1u << p.bits[q]) - 1u)], 1u);
         }
       }
-      // the tile's first-length-digit counts: to tcnt (the ordered-ids fast path's
-      // tile bases, k_radix_tscan) and into the segment histogram
-      __syncthreads();
-      for (int b = t; b < RBINS; b += RT) {
-        const uint32_t c = s_t[b];
-        p.tcnt[(size_t)tile * RBINS + b] = (uint16_t)c;
-        s_h[q0][b] += c;
-        s_t[b] = 0u;
-      }
-      __syncthreads();
     } else {
 #pragma unroll
       for (int j = 0; j < UKEYS; ++j)
         if (j * 32 + lane < nw) {
           const uint32_t dk = (uint32_t)(D[j] < 0 ? 0 : (D[j] > p.max_id ? p.max_id : D[j]));
-          for (int q = q0; q < q1; ++q) atomicAdd(&s_h[q][(dk >> p.shift[q]) & ((1u << p.bits[q]) - 1u)], 1u);
+          atomicAdd(&s_t[(dk >> p.shift[0]) & ((1u << p.bits[0]) - 1u)], 1u);
+          for (int q = 1; q < q1; ++q) atomicAdd(&s_h[q][(dk >> p.shift[q]) & ((1u << p.bits[q]) - 1u)], 1u);
         }
     }
+    // the tile's counts of the first executed digit (ids unordered: the first
+    // id digit, overwriting the upsweep's length counts): to tcnt for
+    // k_radix_tscan, and into the segment histogram
+    __syncthreads();
+    for (int b = t; b < RBINS; b += RT) {
+      const uint32_t c = s_t[b];
+      p.tcnt[(size_t)tile * RBINS + b] = (uint16_t)c;
+      s_h[q0][b] += c;
+      s_t[b] = 0u;
+    }
+    __syncthreads();
   }
   if constexpr (!IDS) {
     if (unsorted) s_unsorted = 1;
@@ -286,22 +287,23 @@ __global__ void __launch_bounds__(RT, 4) k_radix_hist(const __grid_constant__ Ra
 }
 
 // ---------------------------------------------------------------- tile bases
-// Ids already ordered (the first length pass reads the input order the upsweep
-// counted): every tile's per-digit base in its segment is known before the
-// pass, so the pass needs no look-back.  CTA (segment, 32 digits), 1024
+// The first executed pass (the first length pass when ids are ordered, else
+// the first id pass) reads the input order, whose per-tile digit counts the
+// histogram launches wrote to tcnt: every tile's per-digit base in its
+// segment is known before that pass, so it needs no look-back.  CTA (segment, 32 digits), 1024
 // threads: warp w sums its run of tiles per digit (lane), the runs are
 // scanned in shared memory, then each run is walked again writing bases.
 constexpr int TS_T = 1024, TS_W = TS_T / 32;
 __global__ void __launch_bounds__(TS_T) k_radix_tscan(const __grid_constant__ RadixParams p) {
   pdl_wait();
   pdl_trigger();
-  if (*(volatile const int32_t*)p.flags != 0) return;  // ids decrease somewhere: look-back passes
+  const bool unsorted = *(volatile const int32_t*)p.flags != 0;
   __shared__ uint32_t s_run[TS_W][32];
   __shared__ uint32_t s_tot[RBINS];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t seg = blockIdx.x / (RBINS / 32);
   const int d = (int)(blockIdx.x % (RBINS / 32)) * 32 + lane;
-  const int q = p.npass_id;  // the first length pass
+  const int q = unsorted ? 0 : p.npass_id;  // the first executed pass
   const uint32_t* hseg = p.hist + ((size_t)q * p.nseg + seg) * RBINS;
   const int per = (p.tps + TS_W - 1) / TS_W;
   const int k0 = min(w * per, p.tps), k1 = min(k0 + per, p.tps);
@@ -478,7 +480,7 @@ __device__ __forceinline__ void radix_tile(const RadixParams& p, int pass, bool 
   // inclusive prefix at once)
   // ids ordered and this is the first length pass: the tile bases are tabled
   // (k_radix_tscan), no publish and no look-back
-  const bool tabled = !unsorted && pass == p.npass_id;
+  const bool tabled = pass == (unsorted ? 0 : p.npass_id);
   uint32_t* st = p.status[pass & 1] + (size_t)tile * RBINS;
   uint32_t h0 = 0, h1 = 0, tb0 = 0, tb1 = 0;
   if (tabled) {
