@@ -337,6 +337,7 @@ __global__ void __launch_bounds__(TS_T) k_radix_tscan(const __grid_constant__ Ra
   for (int i = 0; i < w; ++i) base += s_run[i][lane];
   uint32_t* tb = p.tbase + (size_t)seg * p.tps * RBINS + d;
   for (int k = k0; k < k1; ++k) {
+    B2_DASSERT(base <= (uint32_t)p.seg_len);
     tb[(size_t)k * RBINS] = base;
     base += tc[(size_t)k * RBINS];
   }
@@ -486,6 +487,7 @@ __device__ __forceinline__ void radix_tile(const RadixParams& p, int pass, bool 
   if (tabled) {
     tb0 = p.tbase[(size_t)tile * RBINS + 2 * t];
     tb1 = p.tbase[(size_t)tile * RBINS + 2 * t + 1];
+    B2_DASSERT(tile < p.ntiles && tb0 + tot[0] <= (uint32_t)p.seg_len && tb1 + tot[1] <= (uint32_t)p.seg_len);
   } else {
 #pragma unroll
     for (int h = 0; h < 2; ++h) st_relaxed_u32(&st[2 * t + h], (tin == 0 ? ST_PRE : ST_AGG) | tot[h]);
