@@ -122,6 +122,20 @@ def test_many_pools_ragged_tiles(seg_len, nseg, lanes):
     check(ids, lens, seg_len, lanes, False, 512, (1 << 20) - 1, with_pos=False)
 
 
+@pytest.mark.parametrize("max_len,lanes,nseg", [(4096, 300, 3), (512, 1, 5), (100_000, 7, 2)])
+def test_ordered_ids_multi_length_pass(max_len, lanes, nseg):
+    """Ids ascending in every pool: the first length pass takes tabled tile bases; with wide lengths
+    the later length passes resolve theirs by look-back.  Lanes > 256 (token sums straight to
+    global memory), one lane (register sums), ragged last tile, many pools."""
+    rng = np.random.default_rng(max_len + lanes)
+    seg_len = lanes * (21_000 // lanes + 1)
+    ids = np.concatenate([np.sort(rng.integers(0, 1 << 24, seg_len)) for _ in range(nseg)])
+    lens = rng.integers(1, max_len + 1, seg_len * nseg)
+    lens[::5] = max_len // 3 + 1  # ties on length
+    check(ids, lens, seg_len, lanes, True, max_len, (1 << 24) - 1)
+    check(ids, lens, seg_len, lanes, False, max_len, (1 << 24) - 1, with_pos=False)
+
+
 def test_full_width_keys_and_sorted_segments():
     """Default bounds (31-bit ids and lengths -> 7 digit passes); ids sorted in some pools only."""
     rng = np.random.default_rng(3)
