@@ -19,6 +19,7 @@ no host synchronisation).
 from __future__ import annotations
 
 import math
+import os
 import threading
 from dataclasses import dataclass
 from enum import Enum
@@ -58,6 +59,7 @@ def capped_bucket_layout(dim: int, bucket_elems: int = BERT_BUCKET_ELEMS) -> tup
 
 _STAGE_ELEMS = 8 << 20  # elements per pinned staging slot (64 MB of fp64; 32 MB slots measured 10 % slower)
 _STAGE_SLOTS = 4
+_STAGE_THREADS = int(os.environ.get("B2_STAGE_THREADS", "8"))  # host threads filling a slot
 _staging: dict = {}
 _staging_lock = threading.Lock()  # one ring per (dtype, device); callers on several threads take turns
 
@@ -90,7 +92,7 @@ def _staged_h2d_locked(flat: torch.Tensor, out: torch.Tensor, key, dtype) -> tor
         st = _staging[key] = {
             "slots": [torch.empty(_STAGE_ELEMS, dtype=dtype).pin_memory() for _ in range(_STAGE_SLOTS)],
             "events": [None] * _STAGE_SLOTS, "stream": torch.cuda.Stream(),
-            "pool": ThreadPoolExecutor(max_workers=8)}
+            "pool": ThreadPoolExecutor(max_workers=_STAGE_THREADS)}
     slots, evs, stream, pool = st["slots"], st["events"], st["stream"], st["pool"]
     dst = out.reshape(-1)
     stream.wait_stream(torch.cuda.current_stream())
@@ -100,7 +102,7 @@ def _staged_h2d_locked(flat: torch.Tensor, out: torch.Tensor, key, dtype) -> tor
         if evs[i] is not None:
             evs[i].synchronize()  # the slot's previous DMA has drained
         buf, m = slots[i], hi - lo
-        step = (m + 7) // 8
+        step = (m + _STAGE_THREADS - 1) // _STAGE_THREADS
         futs = [pool.submit(buf[a:min(m, a + step)].copy_, flat[lo + a:lo + min(m, a + step)])
                 for a in range(0, m, step)]
         for f in futs:
