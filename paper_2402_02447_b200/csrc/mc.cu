@@ -188,7 +188,11 @@ struct McDrawParams {
   int64_t off[kMaxStrataDraw], pop[kMaxStrataDraw], need[kMaxStrataDraw];
   int bits[kMaxStrataDraw];  // log2 of the set size per stratum
   int set_cap, pick_cap;     // shared-memory words for the set and the picks
+  int rbits;                 // compact kernel: value bits above the home slot (entry = probe << rbits | rest)
+  int redo_only;             // 32-bit kernel: only trials the compact kernel marked (out row [0] == kRedo)
+  int pmax_cap;              // > 0: a lower probe-index cap for the compact kernel (tests force the redo path)
 };
+constexpr int32_t kRedo = INT_MIN;  // compact kernel's mark: redo this trial with the 32-bit set
 
 __global__ void __launch_bounds__(32) k_mc_draw(const __grid_constant__ McDrawParams q) {
   // one shared region per trial: the Floyd set, then (reloaded) the picks for
@@ -200,6 +204,7 @@ __global__ void __launch_bounds__(32) k_mc_draw(const __grid_constant__ McDrawPa
   const int lane = threadIdx.x;
   constexpr uint32_t kEmpty = 0xffffffffu;
   for (int64_t tr = blockIdx.x; tr < q.ntrials; tr += gridDim.x) {
+    if (q.redo_only && q.out[tr * q.per_trial] != kRedo) continue;  // warp-uniform
     const uint64_t key = (uint64_t)(q.first_trial + tr);
     rng::Pcg64 g(rng::SeedSeq(q.seed, &key, 1));  // used by lane 0 only
     int64_t row = 0;
@@ -255,6 +260,104 @@ __global__ void __launch_bounds__(32) k_mc_draw(const __grid_constant__ McDrawPa
   }
 }
 
+
+// The same draws with half the shared memory per trial, so twice the trials
+// (independent serial chains) are resident per SM.  The Floyd set holds 16-bit
+// entries: a value's home slot is its low `bits` bits, and the entry keeps
+// the rest of the value (rbits) plus the triangular-probe index at which it
+// was stored, which together give the value back -- membership is exact.  The
+// shuffle permutes 16-bit indices into the picks (numpy's swaps applied to
+// positions), and the gathered lengths land in the same 16-bit slots.  A probe
+// index or a length that does not fit marks the trial (row[0] = kRedo) for
+// the 32-bit kernel, launched behind this one; redoing a trial is always
+// exact, so the marks only cost time.
+__global__ void __launch_bounds__(32) k_mc_draw16(const __grid_constant__ McDrawParams q) {
+  extern __shared__ uint16_t sm16[];
+  const int lane = threadIdx.x;
+  constexpr uint16_t kEmpty16 = 0xffffu;
+  uint32_t pmax = (1u << (16 - q.rbits)) - 2u;  // largest storable probe index (all-ones = empty)
+  if (q.pmax_cap > 0 && (uint32_t)q.pmax_cap < pmax) pmax = (uint32_t)q.pmax_cap;
+  for (int64_t tr = blockIdx.x; tr < q.ntrials; tr += gridDim.x) {
+    const uint64_t key = (uint64_t)(q.first_trial + tr);
+    rng::Pcg64 g(rng::SeedSeq(q.seed, &key, 1));  // used by lane 0 only
+    int64_t row = 0;
+    int redo = 0;
+    for (int k = 0; k < q.nstrata && !redo; ++k) {
+      const int64_t need = q.need[k];
+      if (need == 0) continue;
+      const int bits = q.bits[k];
+      const uint32_t hmask = (1u << bits) - 1u;
+      for (int i = lane; i <= (int)hmask; i += 32) sm16[i] = kEmpty16;
+      __syncwarp();
+      int32_t* o = q.out + tr * q.per_trial + row;
+      if (lane == 0) {
+        const int64_t pop = q.pop[k];
+        for (int64_t j = pop - need; j < pop; ++j) {  // Floyd (numpy _generator choice)
+          const uint32_t val = (uint32_t)g.bounded((uint64_t)j);
+          uint32_t h = val & hmask, i = 0;
+          const uint16_t want = (uint16_t)(val >> bits);
+          bool found = false;
+          for (;;) {  // triangular probing: home + i(i+1)/2 visits every slot
+            if (i > pmax) break;  // entries are stored at probe index <= pmax: not there, and no room
+            const uint16_t e = sm16[h];
+            if (e == kEmpty16) break;
+            if (e == (uint16_t)((i << q.rbits) | want)) {
+              found = true;
+              break;
+            }
+            h = (h + ++i) & hmask;
+          }
+          uint32_t pick = val;
+          if (found) {  // val already drawn: take j itself (never in the set yet)
+            pick = (uint32_t)j;
+            h = pick & hmask;
+            i = 0;
+            while (i <= pmax && sm16[h] != kEmpty16) h = (h + ++i) & hmask;
+          }
+          if (i > pmax) {
+            redo = 1;
+            break;
+          }
+          sm16[h] = (uint16_t)((i << q.rbits) | (pick >> bits));
+          o[j - pop + need] = (int32_t)pick;
+        }
+      }
+      redo = __shfl_sync(0xffffffffu, redo, 0);
+      if (redo) break;
+      // shuffle 16-bit positions instead of the picks: numpy's swaps, same bits
+      for (int64_t i = lane; i < need; i += 32) sm16[i] = (uint16_t)i;
+      __syncwarp();
+      if (lane == 0) {
+        for (int64_t i = need - 1; i >= 1; --i) {  // _shuffle_int(size, 1, idx)
+          const int64_t jj = (int64_t)g.bounded((uint64_t)i);
+          const uint16_t t0 = sm16[jj];
+          sm16[jj] = sm16[i];
+          sm16[i] = t0;
+        }
+      }
+      __syncwarp();
+      // slot i: the pick at position perm[i] -> its length, kept in the same slot
+      const int32_t* L = q.lens + q.off[k];
+      int big = 0;
+      for (int64_t i = lane; i < need; i += 32) {
+        const int32_t v = L[o[sm16[i]]];
+        big |= (uint32_t)v > 0xffffu;
+        sm16[i] = (uint16_t)v;
+      }
+      if (__any_sync(0xffffffffu, big)) {
+        redo = 1;
+        break;
+      }
+      __syncwarp();  // every pick is read before the row is overwritten
+      for (int64_t i = lane; i < need; i += 32) o[i] = (int32_t)sm16[i];
+      __syncwarp();
+      row += need;
+    }
+    if (redo && lane == 0) q.out[tr * q.per_trial] = kRedo;
+    __syncwarp();
+  }
+}
+
 }  // namespace
 }  // namespace b2
 
@@ -301,13 +404,45 @@ extern "C" int b2_mc_draw_device(const int32_t* pool_lens, const int64_t* pool_s
   const size_t smem = sizeof(uint32_t) * (size_t)std::max<int64_t>(q.set_cap, q.pick_cap);
   B2_REQUIRE(smem <= 200 * 1024, B2_ERR_UNSUPPORTED, "trial too large for device draws (%zu B of shared memory)", smem);
   if (ntrials == 0) return B2_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const DeviceInfo& di = device_info();
+  // compact 16-bit set (k_mc_draw16) when every stratum's values leave >= 4 bits of probe index
+  // and positions fit 16 bits; the 32-bit kernel then redoes only the trials it marked
+  static int env16 = -1;
+  if (env16 < 0) {
+    const char* e = getenv("B2_MC_DRAW16");
+    env16 = e ? atoi(e) : 1;
+  }
+  bool compact = env16 != 0 && per > 0;
+  int rbits = 0;
+  for (int k = 0; k < nstrata; ++k) {
+    if (q.need[k] == 0) continue;
+    int vb = 0;  // bits of the largest value, pop - 1
+    while ((1ll << vb) < q.pop[k]) ++vb;
+    rbits = std::max(rbits, std::max(0, vb - q.bits[k]));
+    compact = compact && q.need[k] <= 0xffff;
+  }
+  compact = compact && 16 - rbits >= 4;
+  if (compact) {
+    q.rbits = rbits;
+    const char* pc = getenv("B2_MC_DRAW16_PMAX");  // test hook: force probe overflows -> redo path
+    q.pmax_cap = pc ? atoi(pc) : 0;
+    const size_t smem16 = sizeof(uint16_t) * (size_t)std::max<int64_t>(q.set_cap, q.pick_cap);
+    B2_CHECK(cudaFuncSetAttribute(k_mc_draw16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem16));
+    int occ16 = 0;
+    B2_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ16, k_mc_draw16, 32, smem16));
+    B2_REQUIRE(occ16 >= 1, B2_ERR_UNSUPPORTED, "device draw kernel cannot be resident");
+    const unsigned g16 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntrials, (int64_t)di.sm_count * occ16));
+    k_mc_draw16<<<g16, 32, smem16, st>>>(q);
+    B2_CHECK(cudaGetLastError());
+    q.redo_only = 1;
+  }
   B2_CHECK(cudaFuncSetAttribute(k_mc_draw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
   B2_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mc_draw, 32, smem));
   B2_REQUIRE(occ >= 1, B2_ERR_UNSUPPORTED, "device draw kernel cannot be resident");
-  const DeviceInfo& di = device_info();
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntrials, (int64_t)di.sm_count * occ));
-  k_mc_draw<<<grid, 32, smem, (cudaStream_t)stream>>>(q);
+  k_mc_draw<<<grid, 32, smem, st>>>(q);
   B2_CHECK(cudaGetLastError());
   return B2_OK;
 }

@@ -87,6 +87,22 @@ def test_device_draws_equal_host_draws(case):
     assert np.array_equal(dev.cpu().numpy(), host)
 
 
+@pytest.mark.parametrize("pmax", ["1", "3"])
+def test_device_draws_compact_set_redo_path(pmax, monkeypatch):
+    """The compact (16-bit entry) Floyd set marks a trial whose probe index overflows and the
+    32-bit kernel redoes it: with the probe cap forced down most trials take that path, some
+    don't -- every trial still equals the host draws bit for bit."""
+    from paper_2402_02447_b200.mcsim import draw_trials_device
+
+    lengths = O.generate_lengths(10_000_000, 2402)
+    exp = BalanceExperiment("local_presort", Topology(128, 8), lengths, seed=9, local_batch=16, trials=48)
+    prep = _prepare(exp)
+    want = draw_trials(exp, 3, 48, prep=prep)
+    monkeypatch.setenv("B2_MC_DRAW16_PMAX", pmax)
+    dev = draw_trials_device(exp, 3, 48, prep=prep)
+    assert np.array_equal(dev.cpu().numpy(), want)
+
+
 def test_device_draws_paper_scale_and_tail_shuffle_fallback():
     from paper_2402_02447_b200.mcsim import draw_trials_device, run_trials
 
