@@ -69,7 +69,11 @@ int b2_clip_workspace_init(void* workspace, size_t workspace_bytes, void* stream
  * device arrays of nseg entries.  in_dtype: B2_F32|B2_F64; out_dtype:
  * B2_F32|B2_BF16|B2_F64.  post_scale folds 1/K in when the following
  * collective is a plain sum.  ctas_per_sm <= 0 picks the default.
- * seg_in_off/seg_out_off/seg_len are [host] arrays of nseg int64. */
+ * seg_in_off/seg_out_off/seg_len are [host] arrays of nseg int64.
+ * A lone segment with an output (the DDP-hook / reducer shape) is a
+ * programmatic dependent launch: it may start under the previous kernel of
+ * `stream` and waits for it before reading (B2_CLIP_PDL=0: a plain
+ * cooperative launch). */
 int b2_bucket_clip_cast(const void* in, int in_dtype, void* out, int out_dtype,
                         const int64_t* seg_in_off, const int64_t* seg_out_off,
                         const int64_t* seg_len, int nseg, double limit, double post_scale,
@@ -252,8 +256,9 @@ int b2_presort_deal(const int32_t* ids, const int32_t* lens, int64_t nseg, int s
  * to b2_presort_deal (workspace unused).  When every pool's ids are already
  * non-decreasing (a shard in id order) the id digits are skipped on the
  * device.  `workspace` (device, b2_presort_workspace_bytes(...) bytes; no
- * initialisation needed) holds the key ping-pong buffers, histograms and
- * look-back words.  seg_len < 2^30. */
+ * initialisation needed) holds the key ping-pong buffers, histograms, the
+ * first pass's per-tile digit counts and bases, and look-back words.
+ * seg_len < 2^30. */
 size_t b2_presort_workspace_bytes(int64_t nseg, int seg_len, int32_t max_len, int32_t max_id, int with_pos);
 int b2_presort_sort_deal(const int32_t* ids, const int32_t* lens, int64_t nseg, int seg_len, int lanes, int scan,
                          int32_t max_len, int32_t max_id, int32_t* out_ids, int32_t* out_pos, int64_t* tokens,
@@ -277,7 +282,10 @@ int b2_mc_draw(const int32_t* lengths, const int64_t* pool_sizes, int nstrata, c
  * shuffle), one warp per trial.  pool_lens is device memory (strata
  * concatenated), out is device [ntrials][b*num_gpus].  A stratum in numpy's
  * tail-shuffle branch (pop > 10000 and need > pop/50) -> B2_ERR_UNSUPPORTED
- * (use b2_mc_draw). */
+ * (use b2_mc_draw).  Two launches: a compact-set kernel (16-bit Floyd set,
+ * twice the trials per SM) and the 32-bit kernel for the trials it could not
+ * finish exactly (marked in their first output word); B2_MC_DRAW16=0 runs
+ * the 32-bit kernel alone. */
 int b2_mc_draw_device(const int32_t* pool_lens, const int64_t* pool_sizes, int nstrata, const int64_t* counts,
                       int num_gpus, uint64_t seed, int64_t first_trial, int64_t ntrials, int32_t* out,
                       void* stream);
