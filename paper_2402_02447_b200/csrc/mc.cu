@@ -358,7 +358,6 @@ __global__ void __launch_bounds__(32) k_mc_draw16(const __grid_constant__ McDraw
   }
 }
 
-
 }  // namespace
 }  // namespace b2
 
