@@ -68,6 +68,19 @@ __global__ void __launch_bounds__(kThreads) k_mc_counts(const __grid_constant__ 
   __shared__ int64_t s_mn[kThreads / 32], s_mx[kThreads / 32];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const int b = p.b, G = p.G, P = b * G;
+  // LOCAL_PRESORT: slot i = lane*K + j of a node pool is row i / gpn, column i % gpn of
+  // the trial matrix (offset moff without the node's first column; -1 past the pool), and
+  // sorted position i is dealt to GPU column lnj (snake-flipped on odd rows) -- the same
+  // for every pool and trial, so the divisions are done once
+  int moff[K], lnj[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const int i = lane * K + j;
+    const int gpn = p.gpn > 0 ? p.gpn : 1, r = i / gpn, c = i - r * gpn;
+    const bool in = p.strategy == 2 && i < b * gpn;
+    moff[j] = in ? r * G + c : -1;
+    lnj[j] = in ? ((p.snake && (r & 1)) ? gpn - 1 - c : c) : -1;
+  }
   for (int64_t tr = blockIdx.x; tr < p.ntrials; tr += gridDim.x) {
     const int32_t* m = p.mat + tr * (int64_t)P;
     for (int g = t; g < G; g += kThreads) s_cnt[g] = 0ull;
@@ -83,15 +96,13 @@ __global__ void __launch_bounds__(kThreads) k_mc_counts(const __grid_constant__ 
         s_cnt[g] = (unsigned long long)s;
       }
     } else if (p.strategy == 2) {  // LOCAL_PRESORT: one warp per node pool
-      const int gpn = p.gpn, nodes = G / gpn, PP = b * gpn;
+      const int gpn = p.gpn, nodes = G / gpn;
       for (int nd = w; nd < nodes; nd += kThreads / 32) {
         uint32_t key[K];
 #pragma unroll
         for (int j = 0; j < K; ++j) {
-          const int i = lane * K + j;  // pool order: row r, then the node's columns
-          if (i < PP) {
-            const int r = i / gpn, c = i - r * gpn;
-            const int v = m[(int64_t)r * G + nd * gpn + c];
+          if (moff[j] >= 0) {  // pool order: row r, then the node's columns
+            const int v = m[(int64_t)moff[j] + nd * gpn];
             if (v < 1 || v > p.max_len) *p.bad = 1;
             key[j] = (uint32_t)(p.max_len - v);  // ascending key = descending length
           } else {
@@ -99,14 +110,18 @@ __global__ void __launch_bounds__(kThreads) k_mc_counts(const __grid_constant__ 
           }
         }
         warp_bitonic_sort<K>(key, lane);
+        // the node's column sums by warp reductions: this warp alone owns columns
+        // nd*gpn .. +gpn (plain stores; per-key 64-bit shared atomics into gpn addresses
+        // were half the kernel's time).  A column sum <= b * max_len fits 32 bits.
+        uint32_t lv[K];
 #pragma unroll
-        for (int j = 0; j < K; ++j) {
-          const int pos = lane * K + j;
-          if (pos < PP) {
-            const int r = pos / gpn, c = pos - r * gpn;
-            const int ln = (p.snake && (r & 1)) ? gpn - 1 - c : c;
-            atomicAdd(&s_cnt[nd * gpn + ln], (unsigned long long)(p.max_len - (int)key[j]));
-          }
+        for (int j = 0; j < K; ++j) lv[j] = (uint32_t)(p.max_len - (int)key[j]);
+        for (int col = 0; col < gpn; ++col) {
+          uint32_t part = 0;
+#pragma unroll
+          for (int j = 0; j < K; ++j) part += lnj[j] == col ? lv[j] : 0u;
+          const uint32_t tot = __reduce_add_sync(0xffffffffu, part);
+          if (lane == (col & 31)) s_cnt[nd * gpn + col] = (unsigned long long)tot;
         }
       }
     } else {  // GLOBAL_PRESORT: counting sort of all b*G values
