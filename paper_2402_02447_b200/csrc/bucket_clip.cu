@@ -431,23 +431,33 @@ __global__ void __launch_bounds__(AT + BT, CPS) k_bucket_clip_ws(const __grid_co
     const int gt = t - AT;
     const uint64_t pol_drop = l2_policy_evict_first();
     for (int i = 0, s = gid; s < p.nseg; ++i, s += R) {
+      const Seg sg = p.seg[s];
+      const Tin* in = static_cast<const Tin*>(p.in) + sg.in_off;
+      Tout* out = static_cast<Tout*>(p.out) + sg.out_off;
+      const V* vin = reinterpret_cast<const V*>(in + sg.head);
+      const int64_t v0 = sg.vec ? min64((int64_t)c * sg.per, sg.nv) : 0;
+      const int64_t v1 = sg.vec ? min64(v0 + sg.per, sg.nv) : 0;
+      // the chunk's first UB vectors are loaded before the coefficient is known (they do
+      // not depend on it): their L2 latency overlaps the wait for the bucket's partials
+      V x[UB];
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        const int64_t vi = v0 + gt + (int64_t)u * BT;
+        if (vi < v1) x[u] = ld_b<0>(vin + vi, pol_drop);
+      }
       const double coef = fold(std::integral_constant<int, BT>{}, gt, kBarB, redB, s, c == 0);
       if (gt == 0) s_coef = coef;
       group_sync<BT>(kBarB);
       const Acc cf = static_cast<Acc>(s_coef * p.post_scale);
-      const Seg sg = p.seg[s];
-      const Tin* in = static_cast<const Tin*>(p.in) + sg.in_off;
-      Tout* out = static_cast<Tout*>(p.out) + sg.out_off;
       if (sg.vec) {
-        const V* vin = reinterpret_cast<const V*>(in + sg.head);
         Tout* vout = out + sg.head;
-        const int64_t v0 = min64((int64_t)c * sg.per, sg.nv), v1 = min64(v0 + sg.per, sg.nv);
         for (int64_t v = v0 + gt; v < v1; v += (int64_t)BT * UB) {
-          V x[UB];
+          if (v != v0 + gt) {
 #pragma unroll
-          for (int u = 0; u < UB; ++u) {
-            const int64_t vi = v + (int64_t)u * BT;
-            if (vi < v1) x[u] = ld_b<0>(vin + vi, pol_drop);
+            for (int u = 0; u < UB; ++u) {
+              const int64_t vi = v + (int64_t)u * BT;
+              if (vi < v1) x[u] = ld_b<0>(vin + vi, pol_drop);
+            }
           }
 #pragma unroll
           for (int u = 0; u < UB; ++u) {
