@@ -171,19 +171,28 @@ __global__ void __launch_bounds__(THREADS, CPS) k_bucket_clip_l2lag(const __grid
 
   auto scale_pass = [&](int s) {
     const Seg sg = p.seg[s];
-    const Acc cf = static_cast<Acc>(fold(s, c == 0) * p.post_scale);
     const Tin* in = static_cast<const Tin*>(p.in) + sg.in_off;
     Tout* out = static_cast<Tout*>(p.out) + sg.out_off;
-    if (sg.vec) {
-      const V* vin = reinterpret_cast<const V*>(in + sg.head);
-      Tout* vout = out + sg.head;
-      const int64_t v0 = min64((int64_t)c * sg.per, sg.nv), v1 = min64(v0 + sg.per, sg.nv);
-      for (int64_t v = v0 + t; v < v1; v += (int64_t)THREADS * UB) {
-        V x[UB];
+    const V* vin = reinterpret_cast<const V*>(in + sg.head);
+    const int64_t v0 = sg.vec ? min64((int64_t)c * sg.per, sg.nv) : 0;
+    const int64_t v1 = sg.vec ? min64(v0 + sg.per, sg.nv) : 0;
+    // the chunk's first UB vectors load while the bucket's partials are awaited and folded
+    V x[UB];
 #pragma unroll
-        for (int u = 0; u < UB; ++u) {
-          const int64_t vi = v + (int64_t)u * THREADS;
-          if (vi < v1) x[u] = ld_b<BNC>(vin + vi, pol_drop);
+    for (int u = 0; u < UB; ++u) {
+      const int64_t vi = v0 + t + (int64_t)u * THREADS;
+      if (vi < v1) x[u] = ld_b<BNC>(vin + vi, pol_drop);
+    }
+    const Acc cf = static_cast<Acc>(fold(s, c == 0) * p.post_scale);
+    if (sg.vec) {
+      Tout* vout = out + sg.head;
+      for (int64_t v = v0 + t; v < v1; v += (int64_t)THREADS * UB) {
+        if (v != v0 + t) {
+#pragma unroll
+          for (int u = 0; u < UB; ++u) {
+            const int64_t vi = v + (int64_t)u * THREADS;
+            if (vi < v1) x[u] = ld_b<BNC>(vin + vi, pol_drop);
+          }
         }
 #pragma unroll
         for (int u = 0; u < UB; ++u) {
