@@ -371,15 +371,19 @@ __global__ void __launch_bounds__(AT + BT, CPS) k_bucket_clip_ws(const __grid_co
       // (32 KB per CTA more in flight; the wait overlaps their latency): 370 -> 351 us.
       // With 4 B outputs the extra footprint costs more than it hides (485 -> 515 us), so
       // there the wait comes first.
-      constexpr bool kPreA = sizeof(Tout) <= 2;
-      if constexpr (!kPreA) wait_b();
+      constexpr int kPreA = sizeof(Tout) <= 2 ? UA : UA / 2;  // vectors requested before the wait
       V x[UA];
 #pragma unroll
-      for (int u = 0; u < UA; ++u) {
+      for (int u = 0; u < kPreA; ++u) {
         const int64_t vi = v0 + gt + (int64_t)u * AT;
         x[u] = vi < v1 ? ld_a<0>(vin + vi, pol_keep) : V{};
       }
-      if constexpr (kPreA) wait_b();
+      wait_b();
+#pragma unroll
+      for (int u = kPreA; u < UA; ++u) {
+        const int64_t vi = v0 + gt + (int64_t)u * AT;
+        x[u] = vi < v1 ? ld_a<0>(vin + vi, pol_keep) : V{};
+      }
       double acc[N];
 #pragma unroll
       for (int u = 0; u < N; ++u) acc[u] = 0.0;
