@@ -369,8 +369,8 @@ __global__ void __launch_bounds__(AT + BT, CPS) k_bucket_clip_ws(const __grid_co
       };
       // bf16 out: the chunk's first UA vectors are requested before the L2-footprint wait
       // (32 KB per CTA more in flight; the wait overlaps their latency): 370 -> 351 us.
-      // With 4 B outputs the extra footprint costs more than it hides (485 -> 515 us), so
-      // there the wait comes first.
+      // With 4 B outputs all UA early cost more than they hide (485 -> 515 us); half of
+      // them early measured 485 -> 482 us.
       constexpr int kPreA = sizeof(Tout) <= 2 ? UA : UA / 2;  // vectors requested before the wait
       V x[UA];
 #pragma unroll
