@@ -571,10 +571,11 @@ int launch_ws(ClipParams& p, cudaStream_t stream) {
 // K1 configuration (tools/clip_bench.py sweeps; measurements in DESIGN.md):
 // several buckets per launch -> warp-specialised two-stream kernel
 // (256 norm + 256 scale threads, 8 vectors in flight per thread in both, 2
-// CTAs/SM: 375 us timed alone / 394 us at the power cap vs 382 / 401 for
-// round 1's 192 + 320 with 4 scale vectors, tools/step_timing_probe.py); a
-// lone bucket (DDP-hook shape)
-// -> the time-sliced L2-lag kernel, which has the shorter critical path.
+// CTAs/SM, each stream requesting its next chunk's first vectors before it
+// waits: 351 us timed alone / 378 us at the power cap for BERT-large bf16 out,
+// vs 382 / 401 for round 1's 192 + 320 with 4 scale vectors,
+// tools/step_timing_probe.py); a lone bucket (DDP-hook shape) -> the
+// time-sliced L2-lag kernel, which has the shorter critical path.
 // (The measured alternatives — a TMA shared-memory ring and other warp
 // splits — live in git history, commit 4cd4b3b, not in the product library.)
 template <typename Tin, typename Tout>
